@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the LoPA verify step (liblopa on B200) — BASELINE.json metric
+"LoPA verify-steps/s and logits HBM GB/s (V=151936, k+1 branches) at 1/2/4/8 B200".
+
+A "step" is one pass of the whole hot path (+ a5 at N > 1) over one batch of
+synthetic verify logits: reduce every masked (branch, position) row, score and select, anchor,
+spawn.  Workload (BASELINE configs[1], D2F-Dream shape): V = 151936, W = 32, k = 7 (8 branches),
+tau = 0.9; branch states = the spawn of a fresh fully-masked block after its initial forward;
+logits = SYN-D2F.  Inputs are larger than L2: the timed steps rotate over 8
+logits buffers (622 MB >= 4 x 126 MB L2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lopa|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (branch-parallel, one rank per GPU)
+
+--impl reference times the CPU oracle (oracle/, NumPy fp64) as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "LoPA verify-steps/s and logits HBM GB/s (V=151936,k+1 branches) at 1/2/4/8 B200"
+UNIT = "verify-steps/s"
+CFG = dict(V=151936, W=32, k=7, tau=0.9, seed=1, n_buf=8)
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, device_index: int, period_s: float = 0.002):
+        self.idx, self.period, self.samples, self.reasons = device_index, period_s, [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4): "sw_power_cap",
+            getattr(nv, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake_slowdown",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- workload
+def build_workload(lopa, dev, V, W, k, tau, seed, n_buf, lo=0, hi=None, b_loc=None):
+    """Branch states after the initial forward (a0) of a fresh block, and n_buf copies of their
+    verify logits (branches [lo, hi) only, padded to b_loc rows when sharded)."""
+    st = lopa.Stepper(V, W, k + 1, k, tau, dev)
+    tok = torch.zeros((k + 1, W), dtype=torch.int32, device=dev)
+    msk = torch.zeros((k + 1, W), dtype=torch.uint8, device=dev)
+    msk[0] = 1
+    nb = torch.ones(1, dtype=torch.int32, device=dev)
+    logits0 = torch.zeros((k + 1, W, st.ld), dtype=torch.bfloat16, device=dev)
+    lopa.syn_generate(seed, 0, V, tok, msk, n_branches=1, out=logits0[:1])
+    out = st.step(logits0, nb, tok, msk)
+    torch.cuda.synchronize()
+    tok, msk, nb = out.next_tokens.clone(), out.next_mask.clone(), out.n_next.clone()
+    n = int(nb.item())
+    full = torch.zeros((k + 1, W, st.ld), dtype=torch.bfloat16, device=dev)
+    lopa.syn_generate(seed, 0, V, tok, msk, n_branches=n, out=full[:n])
+    del logits0
+    hi = k + 1 if hi is None else hi
+    rows = (b_loc if b_loc else k + 1)
+    bufs = []
+    for _ in range(n_buf):
+        b = torch.zeros((rows, W, st.ld), dtype=torch.bfloat16, device=dev)
+        if hi > lo:
+            b[: hi - lo] = full[lo:hi]
+        bufs.append(b)
+    torch.cuda.synchronize()
+    masked_rows_total = int(msk[:n].sum().item())
+    local_rows = int(msk[lo:min(hi, n)].sum().item()) if hi > lo else 0
+    return st, tok, msk, nb, full, bufs, masked_rows_total, local_rows
+
+
+def cpu_baseline_oracle(full, tok, msk, nb, k, tau, budget_s=12.0):
+    """The oracle as it stands (NumPy fp64, single thread) on whole verify steps of the same
+    workload, repeated until ~budget_s of CPU time."""
+    from oracle import lopa_oracle as O
+    n = int(nb.item())
+    L16 = full.view(torch.int16).cpu().numpy().view(np.uint16)[:n]
+    t_np, m_np = tok.cpu().numpy()[:n], msk.cpu().numpy()[:n]
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.step(L16, t_np, m_np, k, tau)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return {"value": reps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{reps} full verify steps (n_br={n}, {int(m_np.sum())} masked rows x V=151936) "
+                      f"in {el:.1f} s, NumPy fp64 single thread"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import lopa_oracle as O
+    import syngen
+    V, W, k, tau, seed = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["seed"]
+    # same workload as the liblopa arm, built on the CPU with the NumPy generator
+    tok0, msk0 = syngen.fresh_block(W)
+    L0 = syngen.gen_logits(seed, 0, V, tok0[None], msk0[None])
+    r0 = O.step(L0, tok0[None].astype(np.int64), msk0[None], k, tau)
+    tok, msk = r0.spawn.tokens, r0.spawn.mask
+    L = syngen.gen_logits(seed, 0, V, tok, msk)
+    n_rows = int(msk.sum())
+    # bounded sample per step so that warmup + steps ends in ~2 minutes
+    est = 0.9 * n_rows / 256.0                      # s per full step (1 core)
+    frac = min(1.0, 110.0 / max(1, args.steps + args.warmup) / est)
+    rows = [(j, i) for j in range(len(msk)) for i in range(W) if msk[j, i]]
+    n_s = max(1, int(round(frac * len(rows))))
+    sub = rows[:n_s]
+
+    def one():
+        # a1 on the sampled rows, then a2-a4 on full-size conf (decisions are O(W k))
+        conf = np.full(msk.shape, np.nan)
+        for (j, i) in sub:
+            conf[j, i], _, _ = O.row_confidence(L[j, i])
+        c = np.where(msk.astype(bool), np.nan_to_num(conf, nan=0.5), np.nan)
+        scores = [O.branch_score(c[j], msk[j]) for j in range(len(msk))]
+        w = O.verify_select(scores)
+        a = O.anchor_fill(c[w], np.zeros(W, np.int64), tok[w], msk[w], tau)
+        O.spawn_branches(c[w], np.zeros(W, np.int64), a.tokens, a.mask, k)
+
+    for _ in range(args.warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    el = time.perf_counter() - t0
+    f = n_s / len(rows)
+    value = args.steps * f / el                     # full verify steps per second
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SYN-D2F seeded logits; no weights)",
+            "config": {"workload": "D2F-Dream verify step V=151936 W=32 k=7 tau=0.9 (configs[1])",
+                       "masked_rows": len(rows), "sampled_rows_per_step": n_s},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{n_s} of {len(rows)} masked rows per step (+ full a2-a4), "
+                                       f"scaled by {len(rows)}/{n_s}; NumPy fp64 single thread"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- liblopa arm
+def run_lopa(args):
+    from paper_2512_16229_b200 import lopa
+    import ctypes
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    V, W, k, tau, seed, n_buf = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["seed"], CFG["n_buf"]
+    if world > 1:
+        b_loc, lo, hi = lopa.bp_shard(k + 1, world, rank)
+    else:
+        b_loc, lo, hi = k + 1, 0, k + 1
+    st, tok, msk, nb, full, bufs, rows_total, rows_local = build_workload(
+        lopa, dev, V, W, k, tau, seed, n_buf, lo, hi, b_loc if world > 1 else None)
+    stream = torch.cuda.current_stream(dev)
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    L = lopa.lib()
+
+    bp = None
+    if world > 1:
+        bp = lopa.BranchParallel(st, rank, world)
+
+    # prebuilt argument structs (one per rotating buffer): the timed loop only launches
+    if bp is None:
+        argv = [st.args(b, nb, tok, msk) for b in bufs]
+        refs = [ctypes.byref(a) for a in argv]
+
+        def launch(i):
+            s = L.lopa_step(refs[i % n_buf], sptr)
+            if s:
+                raise lopa.LopaError(f"lopa_step status {s}")
+    else:
+        argv = []
+        for b in bufs:
+            a = st.args(b, nb, tok, msk)
+            a.conf, a.argmax = bp.conf.data_ptr(), bp.argmax.data_ptr()
+            a.workspace, a.workspace_bytes = bp.ws.data_ptr(), bp.ws.numel()
+            a.scores = bp.scores.data_ptr()
+            argv.append(a)
+        refs = [ctypes.byref(a) for a in argv]
+        rec = ctypes.c_void_p(bp.records.data_ptr())
+
+        def launch(i):
+            s = L.lopa_bp_step(bp.h, refs[i % n_buf], bp.b_loc, rec, sptr)
+            if s:
+                raise lopa.LopaError(f"lopa_bp_step status {s}")
+
+    # warm-up
+    for i in range(args.warmup):
+        launch(i)
+    torch.cuda.synchronize()
+
+    # timed region: K steps, an event pair around every step (per-launch kernel time)
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t_start.record(stream)
+        for i in range(K):
+            ev[i][0].record(stream)
+            launch(i)
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    el_ms = t_start.elapsed_time(t_end)
+    per = [a.elapsed_time(b) for a, b in ev]
+    if dist:
+        t = torch.tensor([el_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el_ms = float(t.item())
+    if int(st.out.status.item()) != 0:
+        raise lopa.LopaError(f"device status {int(st.out.status.item())}")
+    if bp is not None:
+        bp.check()
+    value = K / (el_ms / 1000.0)
+    kern_ms = statistics.mean(per)
+    alg_bytes = 2.0 * V * rows_local                 # 2 B per logit of a masked row
+    achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
+    pk = peaks()
+    peak = float(pk.get("hbm_gbs", 6650.0))
+
+    # e2e through the public API with HOST buffers: pinned logits -> device, step, results -> host
+    e2e = None
+    if world == 1:
+        host = full.cpu().pin_memory()
+        h_tok, h_msk, h_nb = tok.cpu().pin_memory(), msk.cpu().pin_memory(), nb.cpu().pin_memory()
+        d_log = torch.empty_like(full)
+        d_tok, d_msk, d_nb = torch.empty_like(tok), torch.empty_like(msk), torch.empty_like(nb)
+        o = st.out
+        h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                 for t in (o.winner, o.scores, o.next_tokens, o.next_mask, o.n_next, o.status)]
+        K2 = max(3, min(K, 50))
+
+        def e2e_step():
+            d_log.copy_(host, non_blocking=True)
+            d_tok.copy_(h_tok, non_blocking=True)
+            d_msk.copy_(h_msk, non_blocking=True)
+            d_nb.copy_(h_nb, non_blocking=True)
+            st.step(d_log, d_nb, d_tok, d_msk, validate=False)
+            for h, t in zip(h_out, (o.winner, o.scores, o.next_tokens, o.next_mask, o.n_next, o.status)):
+                h.copy_(t, non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(K2):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        h2d = full.numel() * 2 + tok.numel() * 4 + msk.numel() + nb.numel() * 4
+        d2h = sum(t.numel() * t.element_size() for t in h_out)
+        e2e = {"value": K2 / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": K2}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline_oracle(full, tok, msk, nb, k, tau)
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tf):
+            try:
+                traffic = json.load(open(tf)).get("bytes_per_launch")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": el_ms / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (SYN-D2F seeded logits; transformer forward out of scope)",
+            "config": {"workload": "D2F-Dream verify step V=151936 W=32 k=7 tau=0.9 (configs[1])",
+                       "branches": int(nb.item()), "masked_rows": rows_total,
+                       "masked_rows_this_rank": rows_local,
+                       "parallelism": f"bp{world}" if world > 1 else "single",
+                       "l2": f"rotating {n_buf} logits buffers ({n_buf * full.numel() * 2 / 1e6:.0f} MB >= 4x L2)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "lopa_reduce_kernel", "kernel_ms_mean": kern_ms,
+                         "alg_bytes_per_launch": alg_bytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "_fallback" not in pk else "fallback"},
+            "logits_gbs_step": alg_bytes / (el_ms / K / 1000.0) / 1e9,
+            "clocks": clk.summary(),
+            "gpu_launches": K * (1 if world == 1 else 2),
+        }
+        if e2e is not None:
+            line["e2e"] = e2e
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if bp is not None:
+        bp.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="lopa", choices=["lopa", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_lopa(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

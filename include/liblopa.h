@@ -1,0 +1,223 @@
+/*
+ * liblopa — the LoPA branch-construction and verification step (arXiv 2512.16229) as a
+ * C-ABI library for NVIDIA B200 (sm_100a).
+ *
+ * Citation keys: P:n = line n of the paper's text; S:n = line n of SPEC.md.
+ * "R<n>" = reading n in DESIGN.md §2 (where the paper is silent or ambiguous).
+ *
+ * What the library computes (one LoPA iteration, Alg. 1, after the forward):
+ *   a1  Conf(i) = top-1 softmax probability of position i's logits, and the greedy token
+ *       ("a confidence function Conf(.) assigns a score to each position i in M_t";
+ *       R1 top-1 probability, R2 temperature 1, R3 greedy, R4 lowest token id on ties).
+ *   a2  Eq. 2 branch confidence C(B_j) = mean of Conf over M_{B_j} (1.0 if
+ *       empty, R8) and B* = argmax_j C(B_j) (ties -> lowest j, anchor first, R9).
+ *   a3  Eq. 1 anchor fill on the winner's reused logits:
+ *       S_high = {i in M : Conf(i) > tau}; I_fill = S_high, else {argmax_i Conf(i)}.
+ *   a4  Alg. 1 step 2: top-k of M_{B0} by (conf desc, position asc) (R6),
+ *       n_br = min(k, |M_{B0}|) + 1 (R7); B_j = B0 with p_j filled by its greedy token.
+ *   a5  Branch parallelism: branches sharded over ranks, one NCCL all-gather of
+ *       each rank's local best (score, id, row) per step.
+ *
+ * Conventions (all calls):
+ *   - Pointers named *_dev / documented "device" are device pointers into caller-owned
+ *     memory.  The library allocates no device memory per call.
+ *   - Every compute call is asynchronous, stream-ordered on `stream` (a cudaStream_t passed
+ *     as void*; NULL = the legacy default stream) and returns a HOST status (lopa_status_t)
+ *     describing argument validation and launch errors only.
+ *   - Data-dependent errors are OR-ed into a caller-zeroed device word `dev_status`
+ *     (LOPA_DEV_*); the host sees them after it synchronises.
+ *   - Logits are bf16, row-major [n_rows][ld] with ld >= vocab, ld % 8 == 0 and a
+ *     16-byte-aligned base (TMA bulk copies move 16-byte units).  Entries in [vocab, ld)
+ *     are never interpreted.
+ *   - Masks are uint8, 1 = masked (position still to be decoded); torch.bool is
+ *     layout-compatible.  Tokens are int32 (V = 151936 > 2^16).
+ *   - Branch tables are [max_branches][window] row-major; branch 0 is the anchor B0.
+ *   - tau is fp32; a position is "high" iff (float)conf > tau (strict; R5, R14).
+ *   - Workspace: lopa_workspace_bytes() bytes of device memory, zeroed by the caller ONCE
+ *     before first use; every successful call leaves its counters zero again.  A workspace
+ *     must not be used by two calls that may run concurrently.  After a LOPA_ERR_CUDA
+ *     return, zero it again.
+ */
+#ifndef LIBLOPA_H_
+#define LIBLOPA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define LOPA_VERSION 10000 /* 1.0.0 */
+
+typedef enum {
+  LOPA_OK = 0,
+  LOPA_ERR_INVALID_ARG = 1, /* null pointer, vocab < 1, window < 1, k < 0, tau not in (0,1],
+                               ld < vocab, ld % 8 != 0, logits not 16-byte aligned, ...   */
+  LOPA_ERR_UNSUPPORTED = 2, /* window > LOPA_MAX_WINDOW, branches > LOPA_MAX_BRANCHES,
+                               rows > LOPA_MAX_ROWS, device is not sm_100                  */
+  LOPA_ERR_CUDA = 3,        /* a CUDA runtime error (launch / capture)                     */
+  LOPA_ERR_NCCL = 4         /* an NCCL error in the branch-parallel exchange               */
+} lopa_status_t;
+
+/* Device status bits (OR-ed into *dev_status). */
+#define LOPA_DEV_EMPTY_MASK 1 /* Eq. 1 applied with nothing masked           */
+#define LOPA_DEV_NONFINITE 2  /* a reduced row holds NaN or +inf, or is all -inf (R20);
+                                 that row's conf / argmax are unspecified                   */
+
+#define LOPA_MAX_WINDOW 64    /* W <= 64: one warp owns a window (NEXT-1 lifts this)        */
+#define LOPA_MAX_BRANCHES 32  /* k + 1 <= 32: one lane per branch in the select             */
+#define LOPA_MAX_ROWS 4096    /* rows per lopa_confidence call                              */
+
+int lopa_version(void);
+const char* lopa_status_string(int status);
+
+/* Bytes of device workspace needed for up to max_rows rows of `vocab` logits. */
+size_t lopa_workspace_bytes(int32_t max_rows, int32_t vocab);
+
+/* Number of canonical segments a row of `vocab` logits is split into (the
+ * fp32 reduction order is fixed per vocab, so conf bits depend only on the row's bytes). */
+int32_t lopa_num_segments(int32_t vocab);
+
+/* a1 — Conf(.) and greedy token of every selected row (R1-R4, R20).
+ *   logits   device bf16 [n_rows][ld]
+ *   row_mask device uint8 [n_rows] or NULL (NULL = reduce every row).  Rows with
+ *            row_mask[r] == 0 are not read and conf[r] / argmax[r] are left untouched.
+ *   conf     device float [n_rows]: 1 / sum_v exp(l_v - max_v l_v)
+ *   argmax   device int32 [n_rows]: the lowest v with l_v = max
+ *   dev_status device int32 (LOPA_DEV_NONFINITE)
+ *   workspace  device, lopa_workspace_bytes(n_rows, vocab) bytes (see conventions)
+ * n_rows = 0 is a no-op.  Errors: INVALID_ARG, UNSUPPORTED (n_rows > LOPA_MAX_ROWS), CUDA. */
+int lopa_confidence(const void* logits, int64_t ld, int32_t n_rows, int32_t vocab,
+                    const uint8_t* row_mask, float* conf, int32_t* argmax, int32_t* dev_status,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* a3 — Eq. 1 + Alg. 1 step 1.
+ *   conf, argmax  device [window] (read only where mask[i] == 1)
+ *   tokens, mask  device [window]: the state x_t, M_t
+ *   tokens_out, mask_out device [window]: B0 (x_{B0}, M_{B0}); may alias tokens / mask.
+ * If nothing is masked: LOPA_DEV_EMPTY_MASK is set and the state is copied unchanged. */
+int lopa_anchor_fill(const float* conf, const int32_t* argmax, const int32_t* tokens,
+                     const uint8_t* mask, int32_t window, float tau, int32_t* tokens_out,
+                     uint8_t* mask_out, int32_t* dev_status, void* stream);
+
+/* a4 — Alg. 1 step 2.
+ *   conf, argmax        device [window] (the anchor's confidences, read where mask_b0 == 1)
+ *   tokens_b0, mask_b0  device [window]
+ *   branch_tokens       device int32 [k+1][window]  (row 0 = B0, row j = B_j)
+ *   branch_mask         device uint8 [k+1][window]
+ *   lookahead_pos       device int32 [k] (p_1..p_n, -1 padded); may be NULL when k == 0
+ *   n_branches          device int32 scalar: n = min(k, |M_B0|) + 1
+ * Rows j > n - 1 of the branch tables are left untouched.  k = 0 is valid (n = 1). */
+int lopa_spawn_branches(const float* conf, const int32_t* argmax, const int32_t* tokens_b0,
+                        const uint8_t* mask_b0, int32_t window, int32_t k,
+                        int32_t* branch_tokens, uint8_t* branch_mask, int32_t* lookahead_pos,
+                        int32_t* n_branches, void* stream);
+
+/* a2 — Eq. 2 + select.
+ *   conf         device float [max_branches][window] (each branch's own verify conf)
+ *   branch_mask  device uint8 [max_branches][window]
+ *   n_branches   device int32 scalar (branches j >= *n_branches are absent)
+ *   scores       device float [max_branches]: C(B_j) (fp64 sum in position order, rounded
+ *                once to fp32); absent branches get -inf
+ *   winner       device int32 scalar: smallest j with the largest fp32 score (R9) */
+int lopa_verify_select(const float* conf, const uint8_t* branch_mask, const int32_t* n_branches,
+                       int32_t max_branches, int32_t window, float* scores, int32_t* winner,
+                       void* stream);
+
+/* One fused verify step (a1 -> a2 -> a3 -> a4) in a single kernel launch. */
+typedef struct {
+  /* inputs */
+  const void* logits;            /* device bf16 [max_branches][window][ld]: verify logits     */
+  int64_t ld;                    /* row stride in elements                                    */
+  int32_t vocab;
+  int32_t window;                /* W <= LOPA_MAX_WINDOW                                      */
+  int32_t max_branches;          /* table capacity (k + 1 for a steady-state loop)           */
+  const int32_t* n_branches;     /* device scalar: branches present in the tables / logits   */
+  const int32_t* branch_tokens;  /* device int32 [max_branches][window]                      */
+  const uint8_t* branch_mask;    /* device uint8 [max_branches][window]                      */
+  int32_t k;                     /* lookahead budget for the next spawn, k + 1 <= LOPA_MAX_BRANCHES */
+  float tau;                     /* Eq. 1 threshold, (0, 1]                                  */
+  /* outputs (device) */
+  float* conf;                   /* [max_branches][window]; written where masked             */
+  int32_t* argmax;               /* [max_branches][window]; written where masked             */
+  float* scores;                 /* [max_branches]                                          */
+  int32_t* winner;               /* scalar j*                                                */
+  int32_t* next_tokens;          /* [k+1][window]: B0..Bn of the next iteration              */
+  uint8_t* next_mask;            /* [k+1][window]                                            */
+  int32_t* lookahead_pos;        /* [k] (may be NULL if k == 0)                              */
+  int32_t* n_branches_next;      /* scalar; 0 = the winner has no masked position (block
+                                    complete, R21): next_tokens[0] / next_mask[0] = winner   */
+  int32_t* dev_status;           /* scalar, LOPA_DEV_* bits                                  */
+  void* workspace;
+  size_t workspace_bytes;        /* >= lopa_workspace_bytes(max_branches * window, vocab)   */
+} lopa_step_args_t;
+
+/* Next tables must not alias the input tables.  Errors: INVALID_ARG, UNSUPPORTED, CUDA. */
+int lopa_step(const lopa_step_args_t* args, void* stream);
+
+/* ---------------------------------------------------------------- branch parallelism (a5)
+ * Global branch j lives on rank j / B_loc, B_loc = ceil(max_branches / world).
+ * Each rank reduces only its branches' logits, scores them, and publishes one record
+ * {its B_loc scores, its best (score, id), that branch's tokens/mask/conf/argmax row}.
+ * One all-gather of the records replaces the (score, id) all-gather + winner-row broadcast
+ * (the broadcast root is device data).  Every rank then runs the same
+ * deterministic select, anchor and spawn, so the next branch tables are replicated.        */
+
+/* Bytes of one rank's exchange record for `window` and `b_loc` local branches. */
+size_t lopa_bp_record_bytes(int32_t window, int32_t b_loc);
+
+/* Local half of a BP step on one rank: a1 + local Eq. 2 + local best -> record.
+ *   args: as lopa_step, except `logits` holds ONLY this rank's branches
+ *         [b_loc][window][ld], conf / argmax are [b_loc][window], and the next_* / winner /
+ *         scores / lookahead / n_branches_next outputs are ignored (may be NULL).
+ *   branch_base: global id of the first local branch (rank * b_loc); b_loc: local capacity.
+ *   record: device, lopa_bp_record_bytes(window, b_loc) bytes. */
+int lopa_bp_local(const lopa_step_args_t* args, int32_t branch_base, int32_t b_loc,
+                  void* record, void* stream);
+
+/* Global half: select over `world` records (contiguous, rank order), then anchor + spawn.
+ * Writes args->scores [world * b_loc >= max_branches] (absent = -inf), winner,
+ * next_tokens / next_mask / lookahead_pos / n_branches_next, dev_status. */
+int lopa_bp_finish(const lopa_step_args_t* args, int32_t b_loc, int32_t world,
+                   const void* records, void* stream);
+
+typedef struct lopa_bp lopa_bp_t;
+#define LOPA_BP_UNIQUE_ID_BYTES 128
+
+/* Rank 0 creates the NCCL unique id; the caller ships it to the other ranks (torch PG). */
+int lopa_bp_get_unique_id(void* unique_id_out /* LOPA_BP_UNIQUE_ID_BYTES */);
+/* Collective over `world` ranks; device = the CUDA device of this rank. */
+int lopa_bp_create(const void* unique_id, int32_t rank, int32_t world, int32_t device,
+                   lopa_bp_t** out);
+/* Full BP step: lopa_bp_local -> ncclAllGather(records) -> lopa_bp_finish, on `stream`.
+ * records: device, world * lopa_bp_record_bytes(window, b_loc) bytes (this rank's slot is
+ * records + rank * record_bytes). */
+int lopa_bp_step(lopa_bp_t* bp, const lopa_step_args_t* args, int32_t b_loc, void* records,
+                 void* stream);
+/* Pending asynchronous NCCL error (ncclCommGetAsyncError), as LOPA_OK / LOPA_ERR_NCCL. */
+int lopa_bp_check(lopa_bp_t* bp);
+void lopa_bp_destroy(lopa_bp_t* bp);
+
+/* ---------------------------------------------------------------- harness (not the method)
+ * SYN-D2F synthetic logits for a batch of branch states (the stand-in for the dLLM forward;
+ * DESIGN.md §3).  Holds none of LoPA's arithmetic.
+ *   branch_tokens / branch_mask device [n_branches][window]; out device bf16 [n_branches]
+ *   [window][ld]; entries in [vocab, ld) are written as 0.  extras: 0 or 1 (toy tie / flat
+ *   rows). */
+int lopa_syn_generate(uint64_t seed, int32_t block, int32_t vocab, int64_t ld, int32_t window,
+                      int32_t n_branches, const int32_t* branch_tokens,
+                      const uint8_t* branch_mask, int32_t extras, void* out, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIBLOPA_H_ */

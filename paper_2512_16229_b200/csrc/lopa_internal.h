@@ -1,0 +1,43 @@
+// Host-side internals shared by the liblopa translation units (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "liblopa.h"
+
+namespace lopa {
+
+// Canonical segmentation of a row: n_seg = ceil(V / 8192) segments of
+// seg_len = 8 * ceil(ceil(V / n_seg) / 8) elements (the last one shorter).  Depends on V only.
+inline void segmentation(int32_t vocab, int32_t* n_seg, int32_t* seg_len) {
+  const int32_t ns = (vocab + 8191) / 8192;
+  const int32_t per = (vocab + ns - 1) / ns;
+  *n_seg = ns;
+  *seg_len = ((per + 7) / 8) * 8;
+}
+
+constexpr int kWarpsPerSeg = 4;  // partials per segment (one per consumer warp)
+
+struct Workspace {
+  uint32_t* done_cnt;   // [1]
+  uint32_t* row_cnt;    // [max_rows]
+  float4* partials;     // [max_rows][n_seg * 4]
+};
+
+size_t workspace_bytes(int32_t max_rows, int32_t vocab);
+bool carve_workspace(void* ws, size_t bytes, int32_t max_rows, int32_t vocab, Workspace* out);
+
+// Selects the device owning `stream` (or `ptr` for the legacy stream) in this library's
+// runtime instance.  Returns false on failure.
+bool bind_device(void* stream, const void* ptr, int* device);
+int num_sms(int device);
+
+inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? LOPA_OK : LOPA_ERR_CUDA; }
+
+int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, const void* records,
+                     cudaStream_t s);
+int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_loc, void* record,
+                    cudaStream_t s);
+int validate_step_args(const lopa_step_args_t* a, bool need_next);
+
+}  // namespace lopa

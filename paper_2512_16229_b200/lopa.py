@@ -1,0 +1,405 @@
+"""Thin ctypes binding of liblopa (include/liblopa.h).  Argument marshalling only: every step of
+the LoPA verify path runs in the library's sm_100a kernels.  PyTorch provides device memory,
+streams and process groups.  There is no CPU fallback: if liblopa.so is missing or the device is
+not a B200 (sm_100), calls raise.
+
+Names follow the paper (arXiv 2512.16229): Conf, Eq. 1 anchor fill,
+lookahead spawn (Alg. 1 step 2), Eq. 2 branch confidence + select.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "liblopa.so")
+
+LOPA_OK = 0
+DEV_EMPTY_MASK = 1
+DEV_NONFINITE = 2
+MAX_WINDOW = 64
+MAX_BRANCHES = 32
+MAX_ROWS = 4096
+UNIQUE_ID_BYTES = 128
+
+_c_void_p = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_f32 = ctypes.c_float
+_size = ctypes.c_size_t
+
+
+class LopaError(RuntimeError):
+    pass
+
+
+class StepArgs(ctypes.Structure):
+    """Mirror of lopa_step_args_t (include/liblopa.h)."""
+    _fields_ = [
+        ("logits", _c_void_p), ("ld", _i64), ("vocab", _i32), ("window", _i32),
+        ("max_branches", _i32), ("n_branches", _c_void_p), ("branch_tokens", _c_void_p),
+        ("branch_mask", _c_void_p), ("k", _i32), ("tau", _f32),
+        ("conf", _c_void_p), ("argmax", _c_void_p), ("scores", _c_void_p), ("winner", _c_void_p),
+        ("next_tokens", _c_void_p), ("next_mask", _c_void_p), ("lookahead_pos", _c_void_p),
+        ("n_branches_next", _c_void_p), ("dev_status", _c_void_p),
+        ("workspace", _c_void_p), ("workspace_bytes", _size),
+    ]
+
+
+_SIGS = {
+    "lopa_version": (_i32, []),
+    "lopa_status_string": (ctypes.c_char_p, [_i32]),
+    "lopa_workspace_bytes": (_size, [_i32, _i32]),
+    "lopa_num_segments": (_i32, [_i32]),
+    "lopa_confidence": (_i32, [_c_void_p, _i64, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
+                               _c_void_p, _c_void_p, _size, _c_void_p]),
+    "lopa_anchor_fill": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _f32,
+                                _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
+    "lopa_spawn_branches": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _i32,
+                                   _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
+    "lopa_verify_select": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i32, _i32, _c_void_p,
+                                  _c_void_p, _c_void_p]),
+    "lopa_step": (_i32, [ctypes.POINTER(StepArgs), _c_void_p]),
+    "lopa_bp_record_bytes": (_size, [_i32, _i32]),
+    "lopa_bp_local": (_i32, [ctypes.POINTER(StepArgs), _i32, _i32, _c_void_p, _c_void_p]),
+    "lopa_bp_finish": (_i32, [ctypes.POINTER(StepArgs), _i32, _i32, _c_void_p, _c_void_p]),
+    "lopa_bp_get_unique_id": (_i32, [_c_void_p]),
+    "lopa_bp_create": (_i32, [_c_void_p, _i32, _i32, _i32, ctypes.POINTER(_c_void_p)]),
+    "lopa_bp_step": (_i32, [_c_void_p, ctypes.POINTER(StepArgs), _i32, _c_void_p, _c_void_p]),
+    "lopa_bp_check": (_i32, [_c_void_p]),
+    "lopa_bp_destroy": (None, [_c_void_p]),
+    "lopa_syn_generate": (_i32, [_u64, _i32, _i32, _i64, _i32, _i32, _c_void_p, _c_void_p, _i32,
+                                 _c_void_p, _c_void_p]),
+}
+EXPORTS = tuple(_SIGS)
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load liblopa.so (built in-tree by paper_2512_16229_b200.build).  Raises if missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise LopaError(f"{LIB_PATH} is not built; run `python -m paper_2512_16229_b200.build` "
+                            "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int, what: str):
+    if st != LOPA_OK:
+        msg = lib().lopa_status_string(st).decode()
+        raise LopaError(f"{what}: liblopa status {st} ({msg})")
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(dev) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise LopaError("liblopa takes CUDA tensors (no CPU fallback)")
+
+
+def _u8(mask: torch.Tensor) -> torch.Tensor:
+    return mask.view(torch.uint8) if mask.dtype == torch.bool else mask
+
+
+def num_segments(vocab: int) -> int:
+    return int(lib().lopa_num_segments(vocab))
+
+
+def workspace_bytes(max_rows: int, vocab: int) -> int:
+    return int(lib().lopa_workspace_bytes(max_rows, vocab))
+
+
+def new_workspace(max_rows: int, vocab: int, device) -> torch.Tensor:
+    """Zeroed device workspace (zero once; the kernels leave it zeroed)."""
+    return torch.zeros(workspace_bytes(max_rows, vocab), dtype=torch.uint8, device=device)
+
+
+def new_status(device) -> torch.Tensor:
+    return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+# ----------------------------------------------------------------------------- a1
+def confidence(logits: torch.Tensor, vocab: int | None = None, row_mask: torch.Tensor | None = None,
+               workspace: torch.Tensor | None = None, status: torch.Tensor | None = None):
+    """Conf and greedy token of each row of bf16 logits [n_rows][ld].
+
+    Returns (conf f32[n_rows], argmax i32[n_rows], status i32[1]); rows not selected by
+    row_mask hold NaN / -1."""
+    _need_cuda(logits, row_mask)
+    if logits.dtype != torch.bfloat16 or logits.dim() != 2 or logits.stride(1) != 1:
+        raise LopaError("logits must be a 2-D bf16 tensor with unit inner stride")
+    n_rows, ld = logits.shape[0], logits.stride(0)
+    vocab = logits.shape[1] if vocab is None else vocab
+    dev = logits.device
+    conf = torch.full((n_rows,), float("nan"), dtype=torch.float32, device=dev)
+    amax = torch.full((n_rows,), -1, dtype=torch.int32, device=dev)
+    status = new_status(dev) if status is None else status
+    if workspace is None:
+        workspace = new_workspace(max(n_rows, 1), vocab, dev)
+    rm = None if row_mask is None else _u8(row_mask).contiguous()
+    _check(lib().lopa_confidence(_p(logits), ld, n_rows, vocab, _p(rm), _p(conf), _p(amax),
+                                 _p(status), _p(workspace), workspace.numel(), _stream(dev)),
+           "lopa_confidence")
+    return conf, amax, status
+
+
+# ----------------------------------------------------------------------------- a3
+def anchor_fill(conf, argmax, tokens, mask, tau: float, status=None):
+    """Eq. 1 + Alg. 1 step 1.  Returns (tokens_B0, mask_B0, status)."""
+    _need_cuda(conf, argmax, tokens, mask)
+    W = mask.numel()
+    dev = mask.device
+    tok_out = torch.empty(W, dtype=torch.int32, device=dev)
+    msk_out = torch.empty(W, dtype=torch.uint8, device=dev)
+    status = new_status(dev) if status is None else status
+    _check(lib().lopa_anchor_fill(_p(conf.contiguous()), _p(argmax.contiguous()),
+                                  _p(tokens.contiguous()), _p(_u8(mask).contiguous()), W, tau,
+                                  _p(tok_out), _p(msk_out), _p(status), _stream(dev)),
+           "lopa_anchor_fill")
+    return tok_out, msk_out, status
+
+
+# ----------------------------------------------------------------------------- a4
+def spawn_branches(conf, argmax, tokens_b0, mask_b0, k: int):
+    """Alg. 1 step 2.  Returns (branch_tokens[k+1][W], branch_mask[k+1][W],
+    lookahead_pos[k], n_branches[1]); rows >= n_branches are zero."""
+    _need_cuda(conf, argmax, tokens_b0, mask_b0)
+    W = mask_b0.numel()
+    dev = mask_b0.device
+    bt = torch.zeros((k + 1, W), dtype=torch.int32, device=dev)
+    bm = torch.zeros((k + 1, W), dtype=torch.uint8, device=dev)
+    look = torch.full((max(k, 1),), -1, dtype=torch.int32, device=dev)
+    nb = torch.zeros(1, dtype=torch.int32, device=dev)
+    _check(lib().lopa_spawn_branches(_p(conf.contiguous()), _p(argmax.contiguous()),
+                                     _p(tokens_b0.contiguous()), _p(_u8(mask_b0).contiguous()),
+                                     W, k, _p(bt), _p(bm), _p(look), _p(nb), _stream(dev)),
+           "lopa_spawn_branches")
+    return bt, bm, look[:k], nb
+
+
+# ----------------------------------------------------------------------------- a2
+def verify_select(conf, branch_mask, n_branches):
+    """Eq. 2 + select.  conf/branch_mask [max_br][W]; n_branches device
+    int32[1].  Returns (scores f32[max_br], winner i32[1])."""
+    _need_cuda(conf, branch_mask, n_branches)
+    max_br, W = branch_mask.shape
+    dev = branch_mask.device
+    scores = torch.empty(max_br, dtype=torch.float32, device=dev)
+    winner = torch.zeros(1, dtype=torch.int32, device=dev)
+    _check(lib().lopa_verify_select(_p(conf.contiguous()), _p(_u8(branch_mask).contiguous()),
+                                    _p(n_branches), max_br, W, _p(scores), _p(winner),
+                                    _stream(dev)),
+           "lopa_verify_select")
+    return scores, winner
+
+
+# ----------------------------------------------------------------------------- fused step
+@dataclass
+class StepOutputs:
+    conf: torch.Tensor          # f32 [max_br][W] (NaN where not reduced)
+    argmax: torch.Tensor        # i32 [max_br][W]
+    scores: torch.Tensor        # f32 [max_br]
+    winner: torch.Tensor        # i32 [1]
+    next_tokens: torch.Tensor   # i32 [k+1][W]
+    next_mask: torch.Tensor     # u8  [k+1][W]
+    lookahead: torch.Tensor     # i32 [max(k,1)]
+    n_next: torch.Tensor        # i32 [1]
+    status: torch.Tensor        # i32 [1]
+
+
+class Stepper:
+    """Owns the workspace and output buffers of `lopa_step` for one (V, W, max_br, k, tau)
+    configuration, so that repeated steps allocate nothing (CUDA-graph friendly)."""
+
+    def __init__(self, vocab: int, window: int, max_branches: int, k: int, tau: float, device,
+                 ld: int | None = None):
+        self.vocab, self.window, self.max_branches, self.k, self.tau = vocab, window, max_branches, k, tau
+        self.ld = ld if ld is not None else ((vocab + 7) // 8) * 8
+        self.device = torch.device(device)
+        d = self.device
+        self.ws = new_workspace(max_branches * window, vocab, d)
+        self.out = StepOutputs(
+            conf=torch.full((max_branches, window), float("nan"), dtype=torch.float32, device=d),
+            argmax=torch.full((max_branches, window), -1, dtype=torch.int32, device=d),
+            scores=torch.empty(max_branches, dtype=torch.float32, device=d),
+            winner=torch.zeros(1, dtype=torch.int32, device=d),
+            next_tokens=torch.zeros((k + 1, window), dtype=torch.int32, device=d),
+            next_mask=torch.zeros((k + 1, window), dtype=torch.uint8, device=d),
+            lookahead=torch.full((max(k, 1),), -1, dtype=torch.int32, device=d),
+            n_next=torch.zeros(1, dtype=torch.int32, device=d),
+            status=new_status(d),
+        )
+
+    def args(self, logits, n_branches, branch_tokens, branch_mask) -> StepArgs:
+        o = self.out
+        return StepArgs(
+            logits=logits.data_ptr(), ld=logits.stride(-2), vocab=self.vocab, window=self.window,
+            max_branches=self.max_branches, n_branches=n_branches.data_ptr(),
+            branch_tokens=branch_tokens.data_ptr(), branch_mask=_u8(branch_mask).data_ptr(),
+            k=self.k, tau=self.tau, conf=o.conf.data_ptr(), argmax=o.argmax.data_ptr(),
+            scores=o.scores.data_ptr(), winner=o.winner.data_ptr(),
+            next_tokens=o.next_tokens.data_ptr(), next_mask=o.next_mask.data_ptr(),
+            lookahead_pos=o.lookahead.data_ptr(), n_branches_next=o.n_next.data_ptr(),
+            dev_status=o.status.data_ptr(), workspace=self.ws.data_ptr(),
+            workspace_bytes=self.ws.numel())
+
+    def _validate(self, logits, n_branches, branch_tokens, branch_mask):
+        _need_cuda(logits, n_branches, branch_tokens, branch_mask)
+        if logits.dtype != torch.bfloat16 or logits.stride(-1) != 1:
+            raise LopaError("logits must be bf16 with unit inner stride")
+        rows = logits.numel() // logits.shape[-1]
+        if rows < self.max_branches * self.window or not logits.is_contiguous():
+            raise LopaError("logits must be contiguous [max_branches][window][ld]")
+        if branch_tokens.dtype != torch.int32 or tuple(branch_tokens.shape) != (self.max_branches, self.window):
+            raise LopaError("branch_tokens must be int32 [max_branches][window]")
+        if tuple(branch_mask.shape) != (self.max_branches, self.window):
+            raise LopaError("branch_mask must be [max_branches][window]")
+
+    def step(self, logits, n_branches, branch_tokens, branch_mask, validate: bool = True) -> StepOutputs:
+        """One fused verify step (a1 -> a2 -> a3 -> a4) in one kernel launch."""
+        if validate:
+            self._validate(logits, n_branches, branch_tokens, branch_mask)
+        a = self.args(logits, n_branches, branch_tokens, branch_mask)
+        _check(lib().lopa_step(ctypes.byref(a), _stream(self.device)), "lopa_step")
+        return self.out
+
+
+# ----------------------------------------------------------------------------- harness
+def syn_cv8(vocab: int) -> int:
+    return 0 if vocab < 2 else int(round(8.0 * math.log(1.8 * (vocab - 1))))
+
+
+def syn_generate(seed: int, block: int, vocab: int, branch_tokens, branch_mask, n_branches=None,
+                 extras: int = 0, ld: int | None = None, out: torch.Tensor | None = None):
+    """SYN-D2F logits (bf16 [n_branches][W][ld]) for the given branch states (harness only)."""
+    _need_cuda(branch_tokens, branch_mask)
+    nb_rows, W = branch_mask.shape
+    n = nb_rows if n_branches is None else n_branches
+    ld = ((vocab + 7) // 8) * 8 if ld is None else ld
+    dev = branch_mask.device
+    if out is None:
+        out = torch.empty((n, W, ld), dtype=torch.bfloat16, device=dev)
+    _check(lib().lopa_syn_generate(seed & ((1 << 64) - 1), block, vocab, ld, W, n,
+                                   _p(branch_tokens.contiguous()), _p(_u8(branch_mask).contiguous()),
+                                   extras, _p(out), _stream(dev)),
+           "lopa_syn_generate")
+    return out
+
+
+# ----------------------------------------------------------------------------- BP (a5)
+def bp_shard(max_branches: int, world: int, rank: int):
+    """Branch-parallel partition: B_loc = ceil(max_branches / world); rank r owns
+    global branches [r * B_loc, min((r + 1) * B_loc, max_branches))."""
+    b_loc = -(-max_branches // world)
+    lo = min(rank * b_loc, max_branches)
+    hi = min(lo + b_loc, max_branches)
+    return b_loc, lo, hi
+
+
+def record_bytes(window: int, b_loc: int) -> int:
+    return int(lib().lopa_bp_record_bytes(window, b_loc))
+
+
+class BranchParallel:
+    """One rank of a branch-parallel LoPA step over NCCL (one process per GPU).
+
+    The NCCL unique id is created by rank 0 and shipped over the given torch process group."""
+
+    def __init__(self, stepper: Stepper, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        self.s, self.rank, self.world = stepper, rank, world
+        self.b_loc, self.lo, self.hi = bp_shard(stepper.max_branches, world, rank)
+        uid = torch.zeros(UNIQUE_ID_BYTES, dtype=torch.uint8)
+        if rank == 0:
+            buf = (ctypes.c_uint8 * UNIQUE_ID_BYTES)()
+            _check(lib().lopa_bp_get_unique_id(buf), "lopa_bp_get_unique_id")
+            uid = torch.tensor(list(buf), dtype=torch.uint8)
+        if world > 1:
+            obj = [uid.tolist()]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = torch.tensor(obj[0], dtype=torch.uint8)
+        raw = (ctypes.c_uint8 * UNIQUE_ID_BYTES)(*uid.tolist())
+        h = ctypes.c_void_p()
+        dev = stepper.device.index if stepper.device.index is not None else torch.cuda.current_device()
+        _check(lib().lopa_bp_create(raw, rank, world, dev, ctypes.byref(h)), "lopa_bp_create")
+        self.h = h
+        W = stepper.window
+        d = stepper.device
+        self.rb = record_bytes(W, self.b_loc)
+        self.records = torch.zeros(world * self.rb, dtype=torch.uint8, device=d)
+        self.ws = new_workspace(self.b_loc * W, stepper.vocab, d)
+        self.conf = torch.full((self.b_loc, W), float("nan"), dtype=torch.float32, device=d)
+        self.argmax = torch.full((self.b_loc, W), -1, dtype=torch.int32, device=d)
+        self.scores = torch.empty(world * self.b_loc, dtype=torch.float32, device=d)
+
+    def step(self, local_logits, n_branches, branch_tokens, branch_mask) -> StepOutputs:
+        """local_logits: this rank's bf16 [b_loc][W][ld]; tables are the full replicated ones."""
+        s = self.s
+        a = s.args(local_logits, n_branches, branch_tokens, branch_mask)
+        a.conf, a.argmax = self.conf.data_ptr(), self.argmax.data_ptr()
+        a.workspace, a.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
+        a.scores = self.scores.data_ptr()
+        _check(lib().lopa_bp_step(self.h, ctypes.byref(a), self.b_loc, _p(self.records),
+                                  _stream(s.device)), "lopa_bp_step")
+        return s.out
+
+    def check(self):
+        _check(lib().lopa_bp_check(self.h), "lopa_bp_check")
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().lopa_bp_destroy(self.h)
+            self.h = None
+
+
+def bp_emulate_step(stepper: Stepper, world: int, logits, n_branches, branch_tokens, branch_mask):
+    """Single-GPU emulation of a `world`-rank BP step: each rank's local half runs on its slice
+    of the logits and writes its record in place, then the global half runs.  Exercises the same
+    kernels as BranchParallel.step minus the NCCL all-gather (whose effect is the identity on
+    the contiguous record array).  Returns (outputs, per-rank local conf list, scores)."""
+    W, d = stepper.window, stepper.device
+    b_loc, _, _ = bp_shard(stepper.max_branches, world, 0)
+    rb = record_bytes(W, b_loc)
+    records = torch.zeros(world * rb, dtype=torch.uint8, device=d)
+    scores = torch.empty(world * b_loc, dtype=torch.float32, device=d)
+    confs = []
+    for r in range(world):
+        _, lo, hi = bp_shard(stepper.max_branches, world, r)
+        local = torch.zeros((b_loc, W, logits.shape[-1]), dtype=logits.dtype, device=d)
+        if hi > lo:
+            local[: hi - lo] = logits[lo:hi]
+        ws = new_workspace(b_loc * W, stepper.vocab, d)
+        conf = torch.full((b_loc, W), float("nan"), dtype=torch.float32, device=d)
+        amax = torch.full((b_loc, W), -1, dtype=torch.int32, device=d)
+        a = stepper.args(local, n_branches, branch_tokens, branch_mask)
+        a.conf, a.argmax, a.workspace, a.workspace_bytes = conf.data_ptr(), amax.data_ptr(), ws.data_ptr(), ws.numel()
+        a.scores = scores.data_ptr()
+        _check(lib().lopa_bp_local(ctypes.byref(a), r * b_loc, b_loc,
+                                   ctypes.c_void_p(records.data_ptr() + r * rb), _stream(d)),
+               "lopa_bp_local")
+        confs.append((conf, amax))
+    a = stepper.args(logits, n_branches, branch_tokens, branch_mask)
+    a.scores = scores.data_ptr()
+    _check(lib().lopa_bp_finish(ctypes.byref(a), b_loc, world, _p(records), _stream(d)),
+           "lopa_bp_finish")
+    return stepper.out, confs, scores
