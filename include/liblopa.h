@@ -203,6 +203,12 @@ int lopa_bp_step(lopa_bp_t* bp, const lopa_step_args_t* args, int32_t b_loc, voi
 int lopa_bp_check(lopa_bp_t* bp);
 void lopa_bp_destroy(lopa_bp_t* bp);
 
+/* Debug: per-CTA phase timeline (%globaltimer ns) of the last reduction launch, for builds
+ * compiled with -DLOPA_TIMELINE; returns the slots per CTA written to out[n_ctas][slots], or 0.
+ * Slots: 0 CTA start, 1 producer start, 2 first stage consumed, 3 last unit consumed,
+ * 4 tail start, 5 tail end. */
+int lopa_debug_timeline(unsigned long long* out, int n_ctas);
+
 /* ---------------------------------------------------------------- harness (not the method)
  * SYN-D2F synthetic logits for a batch of branch states (the stand-in for the dLLM forward;
  * DESIGN.md §3).  Holds none of LoPA's arithmetic.

@@ -41,8 +41,12 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: tuple = ()) -> str:
+    """Build liblopa.so, or liblopa_<variant>.so with extra -D defines (tuning A/B builds;
+    select at run time with LOPA_LIB_VARIANT=<variant>)."""
+    out = LIB if not variant else os.path.join(PKG, f"liblopa_{variant}.so")
+    if not variant and not force and not stale():
         return LIB
     inc, lib = _nccl_dirs()
     cmd = [
@@ -51,16 +55,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
         "-I", os.path.join(ROOT, "include"), "-I", inc,
         *[os.path.join(CSRC, f) for f in SOURCES],
         "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}",
-        "-o", LIB + ".tmp",
+        *[f"-D{d}" for d in defines],
+        "-o", out + ".tmp",
     ]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--variant")
+    ap.add_argument("-D", action="append", default=[])
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, variant=a.variant, defines=tuple(a.D)))

@@ -1,45 +1,95 @@
-// liblopa core: the fused vocabulary reduction (a1) with its in-kernel tails (a2-a4), the
+// liblopa core: the fused vocabulary reduction (a1) with its last-CTA decision tail (a2-a4), the
 // standalone decision kernels and the C-ABI entry points.
 //
-// Kernel design:
-//   * A persistent grid of one CTA per SM.  Work units are (masked row, canonical segment)
-//     pairs, compacted in-kernel from the masks (no host sync) and split into contiguous runs
-//     per CTA, so every SM streams the same number of bytes whatever the row count.
-//   * Warp 0 lane 0 is the TMA producer: one cp.async.bulk of <= 16 KB per unit into an
-//     8-stage shared-memory ring, completion tracked by mbarrier transaction bytes, L2
-//     evict-first (each logit is read exactly once).
-//   * Two consumer warpgroups take alternate stages.  Each of the 4 warps of a group reduces a
-//     fixed interleaved quarter of the segment from shared memory with 128-bit loads: exact
-//     max (max.bf16x2), sum of exp2((x - m) * log2 e) in a fixed tree/sequence, exact first
-//     argmax.  The warp's partial (m, s, argmax) goes to the workspace.
-//   * The warp that completes a row's last partial folds the row's partials in a fixed order
-//     (conf bits depend only on the row's bytes), and the warp that completes the last row
-//     runs the tail: Eq. 2 + select, Eq. 1 anchor, top-k spawn (MODE_STEP) or the local
-//     branch-parallel record (MODE_BP_LOCAL).
+// Fused kernel design:
+//   * Persistent grid, one CTA per SM.  The masked (branch, position) rows are compacted
+//     in-kernel from the masks (no host sync).  A row of V logits is cut into canonical
+//     segments (<= 8192 elements, 16 KB) and segments into canonical groups of kSegPerItem.
+//   * Work items are (row, group) pairs, handed out dynamically: CTA b starts with item b, then
+//     takes the next item from a global counter (prefetched one item ahead), so faster SMs
+//     take more work and all CTAs finish within about one item.
+//   * Warp 0 lane 0 is the TMA producer: one cp.async.bulk per segment into a kStages-deep ring
+//     of 16 KB shared-memory stages, mbarrier transaction-byte completion, L2 evict-first (each
+//     logit is read exactly once).  The stage's (row, segment) tag travels in shared memory.
+//   * kConsumerWGs consumer warpgroups take stages round-robin; the 4 warps of a group each
+//     reduce a fixed interleaved quarter of the segment with 128-bit shared loads: exact max
+//     (max.bf16x2), sum of exp2((x - m) log2 e) with x - m formed exactly by fma.f32.bf16 and
+//     packed f32x2 multiplies/adds in a fixed order, exact first argmax.
+//   * The warp that completes an item folds its 4 x kSegPerItem warp partials (fixed order) into
+//     one group partial in the workspace.  No global atomics per row or per segment.
+//   * The last CTA to finish (one counter) folds every row's group partials in fixed order
+//     (conf bits depend only on the row's bytes), then runs the tail with all its threads:
+//     Eq. 2 scores + select, Eq. 1 anchor, top-k spawn (MODE_STEP) or the local branch-parallel
+//     record (MODE_BP_LOCAL).
 #include <cstdio>
 #include <cstring>
 #include <mutex>
 
 #include "liblopa.h"
+#include "lopa_ptx.cuh"
+namespace lopa {
+// Optional per-CTA timeline (-DLOPA_TIMELINE): %globaltimer stamps of the kernel's phases,
+// read back with lopa_debug_timeline().  Compiled out of the product build.
+#ifdef LOPA_TIMELINE
+constexpr int kTlSlots = 24;
+__device__ unsigned long long g_timeline[256 * kTlSlots];
+__device__ __forceinline__ void tl_stamp(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_timeline[blockIdx.x * kTlSlots + slot] = t;
+}
+#define TL(slot) tl_stamp(slot)
+__device__ __forceinline__ void tl_max(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMax(&g_timeline[blockIdx.x * kTlSlots + slot], t);
+}
+#define TLMAX(slot) tl_max(slot)
+__device__ __forceinline__ void tl_clk(int slot) { g_timeline[blockIdx.x * kTlSlots + slot] = clock64(); }
+__device__ long long g_dbg[8];
+#define DBGC(k) do { if (threadIdx.x == 0) g_dbg[k] = clock64(); } while (0)
+#define TLC(slot) tl_clk(slot)
+#else
+#define TL(slot) ((void)0)
+#define TLMAX(slot) ((void)0)
+#define TLC(slot) ((void)0)
+#define DBGC(k) ((void)0)
+#endif
+}  // namespace lopa
 #include "lopa_decide.cuh"
 #include "lopa_internal.h"
-#include "lopa_ptx.cuh"
 
 namespace lopa {
 
-constexpr int kStages = 8;
-constexpr int kConsumerWGs = 2;
+#ifndef LOPA_STAGES
+#define LOPA_STAGES 6
+#endif
+#ifndef LOPA_WGS
+#define LOPA_WGS 6
+#endif
+#ifndef LOPA_CTAS_PER_SM
+#define LOPA_CTAS_PER_SM 1
+#endif
+constexpr int kStages = LOPA_STAGES;      // TMA ring depth (16 KB stages)
+constexpr int kConsumerWGs = LOPA_WGS;    // consumer warpgroups per CTA
 constexpr int kThreads = 32 + 128 * kConsumerWGs;
 constexpr int kWarps = kThreads / 32;
-constexpr int kStageBytes = 16384;
+constexpr int kStageBytes = kSegPerItem * 2 * kSegElems;  // one work item per stage
 constexpr int kMaxGroups = LOPA_MAX_ROWS / 32;
+constexpr int kPartPerItem = kSegPerItem * kWarpsPerSeg;  // warp partials per work item
+constexpr int kItemSlots = 2 * kStages;                   // item partial slots per CTA
+constexpr int kWgStride = kConsumerWGs / kSegPerItem;     // stages consumed in parallel
+static_assert(kConsumerWGs % kSegPerItem == 0, "warpgroups cover the segments of a stage");
+// A warpgroup must consume every use of its stages in order (mbarrier parity waits can only
+// tell consecutive phases apart), so each stage belongs to exactly one consumer phase.
+static_assert(kStages % kWgStride == 0, "stages must divide evenly among consumer phases");
 
 enum Mode : int { MODE_CONF = 0, MODE_STEP = 1, MODE_BP_LOCAL = 2 };
 
 struct Params {
   const uint16_t* logits;
   int64_t ld;
-  int32_t vocab, n_seg, seg_len;
+  int32_t vocab, n_seg, seg_len, n_grp;  // canonical segmentation (lopa_internal.h)
   int32_t n_cand;              // candidate rows (logits rows)
   const uint8_t* row_mask;     // nullable
   const int32_t* n_branches;   // nullable (MODE_CONF)
@@ -49,9 +99,9 @@ struct Params {
   float* conf;
   int32_t* argmax;
   int32_t* dev_status;
-  uint32_t* done_cnt;
-  uint32_t* row_cnt;
-  float4* partials;
+  uint32_t* ctrs;              // [0] work-item counter, [2] n_masked (K1 -> K2)
+  uint16_t* row_list_out;      // [n_cand] compacted row list (K1 -> K2)
+  float4* gpart;               // [n_cand][n_grp] group partials (m, s, argmax bits, -)
   int mode;
   // tails
   const int32_t* branch_tokens;  // global tables [.. ][W]
@@ -101,6 +151,11 @@ __host__ __device__ inline RecordView record_view(void* base, int32_t b_loc) {
   return v;
 }
 
+// Programmatic dependent launch (PDL): the next kernel in the stream may launch early; its
+// griddepcontrol.wait returns once this grid's memory operations are visible.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // ------------------------------------------------------------------ segment slice reduce
 struct Partial {
   float m, s;
@@ -117,17 +172,33 @@ __device__ __forceinline__ void mask_tail(uint4& v, int nvalid) {
   v = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-__device__ __forceinline__ float chunk_exp_sum(const uint4& v, float m) {
-  // Element order within a 16-byte chunk: e0 = lo(x), e1 = hi(x), e2 = lo(y), ...
-  const float e0 = ex2((bf16lo(v.x) - m) * kLog2e);
-  const float e1 = ex2((bf16hi(v.x) - m) * kLog2e);
-  const float e2 = ex2((bf16lo(v.y) - m) * kLog2e);
-  const float e3 = ex2((bf16hi(v.y) - m) * kLog2e);
-  const float e4 = ex2((bf16lo(v.z) - m) * kLog2e);
-  const float e5 = ex2((bf16hi(v.z) - m) * kLog2e);
-  const float e6 = ex2((bf16lo(v.w) - m) * kLog2e);
-  const float e7 = ex2((bf16hi(v.w) - m) * kLog2e);
-  return ((e0 + e1) + (e2 + e3)) + ((e4 + e5) + (e6 + e7));
+// (lo - m, hi - m) of a bf16x2 word, each formed exactly as one fp32 rounding of x - m:
+// fma.rn.f32.bf16 reads the bf16 halves in place (FHFMA.BF16: no unpack instructions).
+__device__ __forceinline__ float2 minus_m(uint32_t w, float negm) {
+  float lo, hi;
+  asm("{\n.reg .b16 l, h, one;\n"
+      "mov.b32 {l, h}, %2;\n"
+      "mov.b16 one, 0x3F80;\n"
+      "fma.rn.f32.bf16 %0, l, one, %3;\n"
+      "fma.rn.f32.bf16 %1, h, one, %3;\n}"
+      : "=f"(lo), "=f"(hi)
+      : "r"(w), "f"(negm));
+  return make_float2(lo, hi);
+}
+
+__device__ __forceinline__ float2 ex2x2(float2 d) {
+  const float2 z = __fmul2_rn(d, make_float2(kLog2e, kLog2e));
+  return make_float2(ex2(z.x), ex2(z.y));
+}
+
+// Sum of exp(x - m) over one 16-byte chunk (8 elements), in the fixed packed order
+// ((e0,e1) + (e2,e3)) + ((e4,e5) + (e6,e7)) as float2 pairs.
+__device__ __forceinline__ float2 chunk_exp_sum2(const uint4& v, float negm) {
+  const float2 p0 = ex2x2(minus_m(v.x, negm));
+  const float2 p1 = ex2x2(minus_m(v.y, negm));
+  const float2 p2 = ex2x2(minus_m(v.z, negm));
+  const float2 p3 = ex2x2(minus_m(v.w, negm));
+  return __fadd2_rn(__fadd2_rn(p0, p1), __fadd2_rn(p2, p3));
 }
 
 __device__ __forceinline__ bool chunk_has_nan(const uint4& v) {
@@ -140,65 +211,83 @@ __device__ __forceinline__ bool chunk_has_nan(const uint4& v) {
   return bad;
 }
 
-// Warp `wq` (0..3) reduces chunks c = 128 t + 32 wq + lane (t = 0..7) of the stage buffer.
+__device__ __forceinline__ float unordered(uint32_t key) {
+  return __uint_as_float((key & 0x80000000u) ? (key & 0x7FFFFFFFu) : ~key);
+}
+
+// Warp `wq` (0..3) reduces chunks c = 128 t + 32 wq + lane (t = 0..7) of the stage buffer and
+// releases the stage (empty_bar) once its shared-memory reads are done.
 // e0: row element index of the segment's first element.
 __device__ __forceinline__ Partial reduce_slice(const uint8_t* stage, int nchunks, int e0,
-                                                int vocab, int wq, int lane) {
+                                                int vocab, int wq, int lane, uint64_t* empty_bar) {
   const uint4* buf = reinterpret_cast<const uint4*>(stage);
-  uint4 v[8];
+  uint4 v[kChunksPerLane];
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {
+  for (int t = 0; t < kChunksPerLane; ++t) {
     const int c = 128 * t + 32 * wq + lane;
     v[t] = (c < nchunks) ? lds128(buf + c)
                          : make_uint4(kNegInfBf16x2, kNegInfBf16x2, kNegInfBf16x2, kNegInfBf16x2);
   }
-  if ((vocab & 7) != 0) {
+#ifdef LOPA_NOCOMPUTE
+  // streaming experiment: consume the stage and return a dummy partial
+  {
+    uint32_t acc = 0;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int t = 0; t < kChunksPerLane; ++t) acc ^= v[t].x ^ v[t].y ^ v[t].z ^ v[t].w;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar);
+    Partial d;
+    d.m = 0.f;
+    d.s = 1.0f + (acc == 0x12345678u ? 1.f : 0.f);
+    d.a = 0;
+    return d;
+  }
+#endif
+  const bool ragged = (vocab & 7) != 0;
+  if (ragged) {
+#pragma unroll
+    for (int t = 0; t < kChunksPerLane; ++t) {
       const int c = 128 * t + 32 * wq + lane;
       const int nvalid = vocab - (e0 + 8 * c);
       if (c < nchunks && nvalid < 8) mask_tail(v[t], nvalid);
     }
   }
   // exact max: per-chunk bf16x2 max, then across chunks and lanes
-  uint32_t cm[8];
+  uint32_t cm[kChunksPerLane];
 #pragma unroll
-  for (int t = 0; t < 8; ++t) cm[t] = bmax2(bmax2(v[t].x, v[t].y), bmax2(v[t].z, v[t].w));
+  for (int t = 0; t < kChunksPerLane; ++t) cm[t] = bmax2(bmax2(v[t].x, v[t].y), bmax2(v[t].z, v[t].w));
   uint32_t mm = cm[0];
 #pragma unroll
-  for (int t = 1; t < 8; ++t) mm = bmax2(mm, cm[t]);
+  for (int t = 1; t < kChunksPerLane; ++t) mm = bmax2(mm, cm[t]);
   const float ml = fmaxf(bf16lo(mm), bf16hi(mm));
-  const uint32_t okey = __reduce_max_sync(0xffffffffu, ordered_bits(ml));
-  const float m = __uint_as_float((okey & 0x80000000u) ? (okey & 0x7FFFFFFFu) : ~okey);
+  const float m = unordered(__reduce_max_sync(0xffffffffu, ordered_bits(ml)));
 
   Partial p;
   p.m = m;
   if (m == -INFINITY) {  // warp-uniform: every element is -inf (or NaN)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar);
     bool bad = false;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) bad |= chunk_has_nan(v[t]);
+    for (int t = 0; t < kChunksPerLane; ++t) bad |= chunk_has_nan(v[t]);
     p.s = __any_sync(0xffffffffu, bad) ? __int_as_float(0x7FC00000) : 0.f;
     p.a = 0xFFFFFFFFu;
     return p;
   }
-  // sum of exp in a fixed order: tree inside a chunk, chunks in t order, butterfly over lanes
-  float ls = 0.f;
-#pragma unroll
-  for (int t = 0; t < 8; ++t) ls += chunk_exp_sum(v[t], m);
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
-  p.s = ls;
-  // exact first argmax: only lanes holding the max search their registers
+  // exact first argmax: a lane holding the max finds its first chunk containing it and re-reads
+  // that chunk from shared memory (the stage is released only afterwards).
   uint32_t cand = 0xFFFFFFFFu;
   if (ml == m) {
-    int tf = 7;
+    int tf = kChunksPerLane - 1;
 #pragma unroll
-    for (int t = 7; t >= 0; --t)
+    for (int t = kChunksPerLane - 1; t >= 0; --t)
       if (fmaxf(bf16lo(cm[t]), bf16hi(cm[t])) == m) tf = t;
-    uint4 w = v[0];
-#pragma unroll
-    for (int t = 1; t < 8; ++t)
-      if (tf == t) w = v[t];
+    const int c = 128 * tf + 32 * wq + lane;
+    uint4 w = lds128(buf + c);
+    if (ragged) {
+      const int nvalid = vocab - (e0 + 8 * c);
+      if (nvalid < 8) mask_tail(w, nvalid);
+    }
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
     int ef = 7;
 #pragma unroll
@@ -206,119 +295,285 @@ __device__ __forceinline__ Partial reduce_slice(const uint8_t* stage, int nchunk
       const float x = (e & 1) ? bf16hi(ws[e >> 1]) : bf16lo(ws[e >> 1]);
       if (x == m) ef = e;
     }
-    cand = (uint32_t)(e0 + 8 * (128 * tf + 32 * wq + lane) + ef);
+    cand = (uint32_t)(e0 + 8 * c + ef);
   }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_bar);
   p.a = __reduce_min_sync(0xffffffffu, cand);
+  // sum of exp(x - m) in a fixed order: packed tree inside a chunk, chunks in t order, then
+  // (.x + .y), then a butterfly over lanes (identical bits in every lane)
+  const float negm = -m;
+  float2 acc = chunk_exp_sum2(v[0], negm);
+#pragma unroll
+  for (int t = 1; t < kChunksPerLane; ++t) acc = __fadd2_rn(acc, chunk_exp_sum2(v[t], negm));
+  float ls = acc.x + acc.y;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
+  p.s = ls;
   return p;
 }
 
-// Fold a row's partials (fixed order: lane-sequential over p = lane, lane + 32, ..., then a
-// butterfly) -> conf, argmax.  Returns true if the row is not a distribution (R20).
-__device__ __forceinline__ bool fold_row(const float4* P, int n_part, int lane, float* conf_out,
-                                         int32_t* amax_out) {
-  float ml = -INFINITY;
-  for (int p = lane; p < n_part; p += 32) ml = fmaxf(ml, __ldcg(P + p).x);
-  const uint32_t okey = __reduce_max_sync(0xffffffffu, ordered_bits(ml));
-  const float M = __uint_as_float((okey & 0x80000000u) ? (okey & 0x7FFFFFFFu) : ~okey);
-  float S = 0.f;
-  uint32_t a = 0xFFFFFFFFu;
-  for (int p = lane; p < n_part; p += 32) {
-    const float4 q = __ldcg(P + p);
-    S += q.y * ex2((q.x - M) * kLog2e);
-    if (q.x == M) a = min(a, __float_as_uint(q.z));
+// ------------------------------------------------------------------ canonical folds
+// Fold of partials q[0..n) in index order: M = max m; S = sum_p s_p * 2^((m_p - M) log2 e) in p
+// order; argmax = the smallest index among partials with m_p = M.  A partial whose max is -inf
+// contributes 0 (or NaN if it saw a NaN); a fold whose max is -inf has S = 0 (or NaN).
+struct FoldAcc {
+  float M, S;
+  uint32_t a;
+};
+template <typename Get>
+__device__ __forceinline__ FoldAcc fold_seq(int n, Get get) {
+  float M = -INFINITY;
+#pragma unroll 1
+  for (int p = 0; p < n; ++p) M = fmaxf(M, get(p).x);
+  FoldAcc r{M, 0.f, 0xFFFFFFFFu};
+#pragma unroll 1
+  for (int p = 0; p < n; ++p) {
+    const float4 q = get(p);
+    if (q.x == -INFINITY || M == -INFINITY) {
+      r.S += isnan(q.y) ? q.y : 0.f;
+    } else {
+      r.S += q.y * ex2((q.x - M) * kLog2e);
+      if (q.x == M) r.a = min(r.a, __float_as_uint(q.z));
+    }
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
-  a = __reduce_min_sync(0xffffffffu, a);
-  *conf_out = __fdiv_rn(1.0f, S);
-  *amax_out = (int32_t)a;
-  return !(S >= 1.0f);
+  return r;
 }
 
-// ------------------------------------------------------------------ tails (one warp)
-__device__ void tail_step(const Params& P, uint64_t* keys, int lane) {
-  __threadfence();
+// Row fold over <= 16 group partials held in registers: M = max (order-free); the terms are
+// summed in a fixed 16-slot pairwise tree (slots >= n hold +0, which leaves every sum exact),
+// so the result depends only on the partials; argmax = smallest index among partials with m = M.
+__device__ __forceinline__ FoldAcc fold_tree16(int n, const float4 (&q)[16]) {
+  float M = -INFINITY;
+#pragma unroll
+  for (int p = 0; p < 16; ++p)
+    if (p < n) M = fmaxf(M, q[p].x);
+  float t[16];
+  uint32_t a = 0xFFFFFFFFu;
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    t[p] = 0.f;
+    if (p < n) {
+      if (q[p].x == -INFINITY || M == -INFINITY) {
+        t[p] = isnan(q[p].y) ? q[p].y : 0.f;
+      } else {
+        t[p] = q[p].y * ex2((q[p].x - M) * kLog2e);
+        if (q[p].x == M) a = min(a, __float_as_uint(q[p].z));
+      }
+    }
+  }
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+    for (int p = 0; p < w; ++p) t[p] = t[2 * p] + t[2 * p + 1];
+  return FoldAcc{M, t[0], a};
+}
+
+// ------------------------------------------------------------------ last-CTA tail
+// Everything the decision tail needs, staged in the (idle) TMA ring of the last CTA.
+struct TailSmem {
+  float conf[LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW];
+  int32_t amax[LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW];
+  int32_t tok[LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW];
+  uint8_t msk[LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW];
+  float scores[LOPA_MAX_BRANCHES];
+  uint64_t keys[LOPA_MAX_WINDOW];
+  int32_t b0_tok[LOPA_MAX_WINDOW];
+  int32_t b0_amax[LOPA_MAX_WINDOW];
+  uint8_t b0_msk[LOPA_MAX_WINDOW];
+  int32_t rank[LOPA_MAX_WINDOW];
+  int32_t n;       // lookahead count, -1 = winner complete
+  int32_t best;    // (BP) local best
+};
+constexpr size_t kTailBytes = (sizeof(TailSmem) + 127) / 128 * 128;
+
+// Eq. 2 for branches [0, cap) of the staged table (nb present): warp w scores w, w + kWarps, ...
+// The fp64 sum of <= 64 confidences, each >= 1/V >= 2^-23, is exact in any order.
+template <int NT>
+__device__ __forceinline__ void cta_scores(TailSmem& T, int cap, int nb, int W, int warp,
+                                           int lane, float* out) {
+  for (int j = warp; j < cap; j += NT / 32) {
+    double s = 0.0;
+    int c = 0;
+    if (j < nb) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = lane + 32 * h;
+        if (i < W) {
+          s += (double)T.conf[j * W + i];
+          c += T.msk[j * W + i];
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, off);
+      c += __shfl_xor_sync(0xffffffffu, c, off);
+    }
+    if (lane == 0) {
+      const float sc = j < nb ? (c ? (float)(s / (double)c) : 1.0f) : -INFINITY;
+      T.scores[j] = sc;
+      if (out) out[j] = sc;
+    }
+  }
+}
+
+// a2 -> a3 -> a4 with all NT threads of the tail CTA (T.conf / T.amax hold the folded rows).
+template <int NT>
+__device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
+  const int warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
   const int nb = max(0, min(*P.n_branches, P.cap));
-  const float score = warp_branch_score(P.conf, P.branch_mask, nb, P.cap, W, lane);
-  if (lane < P.cap) P.scores[lane] = score;
-  const int w = warp_select(score, lane, nb);
-  if (lane == 0) *P.winner = w;
-  WinRegs r;
-  load_window(r, P.conf + (size_t)w * W, P.argmax + (size_t)w * W,
-              P.branch_tokens + (size_t)w * W, P.branch_mask + (size_t)w * W, W, lane);
-  const bool any = __ballot_sync(0xffffffffu, r.msk[0] | r.msk[1]) != 0;
-  if (!any) {  // R21: the winner is complete
-    store_window(r, P.next_tokens, P.next_mask, W, lane);
+  cta_scores<NT>(T, P.cap, nb, W, warp, lane, P.scores);
+  __syncthreads();
+  TL(7);
+  if (warp == 0) {
+    const float sc = lane < P.cap ? T.scores[lane] : -INFINITY;
+    const int w = warp_select(sc, lane, nb);
+    WinRegs r;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = lane + 32 * h;
+      const bool in = i < W;
+      r.msk[h] = in ? (uint32_t)T.msk[w * W + i] : 0u;
+      r.tok[h] = in ? T.tok[w * W + i] : 0;
+      r.conf[h] = in ? T.conf[w * W + i] : 0.f;
+      r.amax[h] = in ? T.amax[w * W + i] : -1;
+    }
+    const bool any = __ballot_sync(0xffffffffu, r.msk[0] | r.msk[1]) != 0;
+    if (any) warp_anchor(r, P.tau, lane);
+    int n_mb0 = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = lane + 32 * h;
+      T.b0_tok[i] = r.tok[h];
+      T.b0_amax[i] = r.amax[h];
+      T.b0_msk[i] = (uint8_t)r.msk[h];
+      T.keys[i] = r.msk[h] ? (((uint64_t)ordered_bits(r.conf[h]) << 32) | (uint64_t)(63 - i)) : 0ull;
+      n_mb0 += __popc(__ballot_sync(0xffffffffu, r.msk[h]));
+    }
+    if (lane == 0) {
+      *P.winner = w;
+      T.n = any ? min(P.k, n_mb0) : -1;
+    }
+  }
+  __syncthreads();
+  TL(9);
+  const int nl = T.n;
+  if (nl < 0) {  // R21: the winner is complete -> pass it through, no branches
+    for (int i = tid; i < W; i += NT) {
+      P.next_tokens[i] = T.b0_tok[i];
+      P.next_mask[i] = T.b0_msk[i];
+    }
     if (P.lookahead)
-      for (int q = lane; q < P.k; q += 32) P.lookahead[q] = -1;
-    if (lane == 0) *P.n_next = 0;
+      for (int q = tid; q < P.k; q += NT) P.lookahead[q] = -1;
+    if (tid == 0) *P.n_next = 0;
     return;
   }
-  warp_anchor(r, P.tau, lane);
-  warp_spawn(r, W, P.k, keys, P.next_tokens, P.next_mask, P.lookahead, P.n_next, lane);
+  // Alg. 1 step 2: rank of each position of M_B0 under (conf desc, position asc)
+  // (4 threads per position, 16 keys each, combined with two shuffles)
+  if (tid < 4 * LOPA_MAX_WINDOW) {
+    const int pos = tid >> 2, part = tid & 3;
+    const uint64_t mine = T.keys[pos];
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) cnt += (T.keys[16 * part + q] > mine) ? 1 : 0;
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+    if (part == 0) {
+      const int rk = T.b0_msk[pos] ? cnt : (1 << 20);
+      T.rank[pos] = rk;
+      if (rk < nl && P.lookahead) P.lookahead[rk] = pos;
+    }
+  }
+  if (P.lookahead)
+    for (int q = nl + tid; q < P.k; q += NT) P.lookahead[q] = -1;
+  __syncthreads();
+  TL(12);
+  const int total = (nl + 1) * W;
+  for (int idx = tid; idx < total; idx += NT) {
+    const int j = idx / W, i = idx - j * W;
+    const bool fill = (j >= 1) && (T.rank[i] == j - 1);
+    P.next_tokens[idx] = fill ? T.b0_amax[i] : T.b0_tok[i];
+    P.next_mask[idx] = fill ? (uint8_t)0 : T.b0_msk[i];
+  }
+  if (tid == 0) *P.n_next = nl + 1;
+  TL(13);
 }
 
-__device__ void tail_bp_local(const Params& P, int lane) {
-  __threadfence();
+// Local half of a BP step with all threads of the last CTA: local Eq. 2 scores, local best
+// (smallest local j with the largest score), and the exchange record.
+template <int NT>
+__device__ void cta_tail_bp_local(const Params& P, TailSmem& T, int tid) {
+  const int warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
   const int nb = max(0, min(*P.n_branches - P.branch_base, P.cap));
-  const uint8_t* bmask = P.branch_mask + (size_t)P.branch_base * W;
-  const float score = warp_branch_score(P.conf, bmask, nb, P.cap, W, lane);
   RecordView rv = record_view(P.record, P.cap);
-  if (lane < P.cap) rv.scores[lane] = score;
-  const int w = warp_select(score, lane, nb);
-  const float best = __shfl_sync(0xffffffffu, score, w);
-  if (lane == 0) {
-    *rv.best_score = nb > 0 ? best : -INFINITY;
-    *rv.best_id = nb > 0 ? P.branch_base + w : 0x7FFFFFFF;
-    *rv.n_present = nb;
-    *rv.b_loc = P.cap;
+  cta_scores<NT>(T, P.cap, nb, W, warp, lane, rv.scores);
+  __syncthreads();
+  if (warp == 0) {
+    const float sc = lane < P.cap ? T.scores[lane] : -INFINITY;
+    const int w = warp_select(sc, lane, nb);
+    if (lane == 0) {
+      *rv.best_score = nb > 0 ? T.scores[w] : -INFINITY;
+      *rv.best_id = nb > 0 ? P.branch_base + w : 0x7FFFFFFF;
+      *rv.n_present = nb;
+      *rv.b_loc = P.cap;
+      T.best = w;
+    }
   }
-  if (nb == 0) return;
-  WinRegs r;
-  load_window(r, P.conf + (size_t)w * W, P.argmax + (size_t)w * W,
-              P.branch_tokens + (size_t)(P.branch_base + w) * W, bmask + (size_t)w * W, W, lane);
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int i = lane + 32 * s;
-    rv.tokens[i] = r.tok[s];
-    rv.conf[i] = r.conf[s];
-    rv.argmax[i] = r.amax[s];
-    rv.mask[i] = (uint8_t)r.msk[s];
+  __syncthreads();
+  const int w = T.best;
+  for (int i = tid; i < LOPA_MAX_WINDOW; i += NT) {
+    const bool in = i < W && nb > 0;
+    rv.tokens[i] = in ? T.tok[w * W + i] : 0;
+    rv.conf[i] = in ? T.conf[w * W + i] : 0.f;
+    rv.argmax[i] = in ? T.amax[w * W + i] : -1;
+    rv.mask[i] = in ? T.msk[w * W + i] : (uint8_t)0;
   }
 }
 
 // ------------------------------------------------------------------ the fused kernel
-__global__ void __launch_bounds__(kThreads, 1) lopa_reduce_kernel(const Params P) {
+__global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel(const Params P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* stages = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  uint32_t* gbits = reinterpret_cast<uint32_t*>(empty + kStages);
+  uint64_t* slot_free = empty + kStages;
+  int4* stage_info = reinterpret_cast<int4*>(slot_free + kItemSlots);
+  float4* ipart = reinterpret_cast<float4*>(stage_info + kStages);  // [kItemSlots][kPartPerItem]
+  uint32_t* icnt = reinterpret_cast<uint32_t*>(ipart + kItemSlots * kPartPerItem);
+  uint32_t* gbits = icnt + kItemSlots;
   uint32_t* goff = gbits + kMaxGroups;
-  uint32_t* misc = goff + kMaxGroups;  // [0] = n_masked
+  uint32_t* misc = goff + kMaxGroups;  // [0] = n_masked, [1] = last-CTA flag
   uint16_t* row_list = reinterpret_cast<uint16_t*>(misc + 4);
-  uint64_t* keys = reinterpret_cast<uint64_t*>(row_list + LOPA_MAX_ROWS);  // [kWarps][64]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) TL(0);
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kWarpsPerSeg);
+      mbar_init(&empty[s], kWarpsPerSeg * kSegPerItem);
     }
+    for (int q = 0; q < kItemSlots; ++q) mbar_init(&slot_free[q], 1);
     fence_mbar_init();
   }
+  for (int q = tid; q < kItemSlots; q += kThreads) icnt[q] = 0;
+  // PDL: wait for the previous kernel's writes (e.g. the previous step's tables) before touching
+  // global inputs, then let the dependent fold/tail kernel launch (it may prefetch the inputs).
+  grid_dep_wait();
+  grid_dep_launch();
   // ---- in-kernel row compaction: rows with mask = 1 of present branches
   const int W = P.window;
-  int nb_eff = 0x7FFFFFFF;
-  if (P.n_branches) nb_eff = *P.n_branches - P.branch_base;
   const int n_groups = (P.n_cand + 31) >> 5;
   for (int g = warp; g < n_groups; g += kWarps) {
     const int r = g * 32 + lane;
-    bool v = r < P.n_cand;
-    if (v && P.row_mask) v = P.row_mask[r] != 0;
+    // the mask byte and n_branches are loaded independently (one round trip)
+    const bool in = r < P.n_cand;
+    const bool mk = (in && P.row_mask) ? P.row_mask[r] != 0 : in;
+    const int nb_eff = P.n_branches ? *P.n_branches - P.branch_base : 0x7FFFFFFF;
+    bool v = mk;
     if (v && P.n_branches) v = (r / W) < nb_eff;
     const uint32_t bits = __ballot_sync(0xffffffffu, v);
     if (lane == 0) gbits[g] = bits;
@@ -357,93 +612,255 @@ __global__ void __launch_bounds__(kThreads, 1) lopa_reduce_kernel(const Params P
   __syncthreads();
 
   const int n_masked = (int)misc[0];
-  if (n_masked == 0) {
-    if (blockIdx.x == 0 && warp == 1) {
-      if (P.mode == MODE_STEP) tail_step(P, keys + 64 * warp, lane);
-      if (P.mode == MODE_BP_LOCAL) tail_bp_local(P, lane);
-    }
-    return;
-  }
-  const int n_seg = P.n_seg;
-  const int n_part = n_seg * kWarpsPerSeg;
-  const long long U = (long long)n_masked * n_seg;
-  const long long u0 = U * blockIdx.x / gridDim.x;
-  const long long u1 = U * (blockIdx.x + 1) / gridDim.x;
-  const int n_local = (int)(u1 - u0);
+  const int n_seg = P.n_seg, n_grp = P.n_grp;
+  const int n_items = n_masked * n_grp;
+  const int G = (int)gridDim.x;
 
   if (warp == 0) {
-    // ---- TMA producer
     if (lane == 0) {
+      // ---- TMA producer: items blockIdx.x, then G + counter, ...
       const uint64_t pol = policy_evict_first();
-      for (int i = 0; i < n_local; ++i) {
-        const long long u = u0 + i;
-        const int rc = (int)(u / n_seg);
-        const int seg = (int)(u - (long long)rc * n_seg);
+      TL(1);
+      uint32_t i = 0;  // item (= stage use) sequence number of this CTA
+      // Issue one work item (row rc, group g): ONE bulk copy of its <= kSegPerItem segments.
+      auto issue = [&](int cur) {
+        const int rc = cur / n_grp, g = cur - rc * n_grp;
         const int row = row_list[rc];
-        const int s = i % kStages;
-        if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
-        const int e0 = seg * P.seg_len;
-        const int e1 = min(P.vocab, e0 + P.seg_len);
+        const int s0 = g * kSegPerItem, s1 = min(n_seg, s0 + kSegPerItem);
+        const int slot = (int)(i % kItemSlots);
+        if (i >= (uint32_t)kItemSlots) mbar_wait(&slot_free[slot], ((i / kItemSlots) - 1) & 1);
+        const int s = (int)(i % kStages);
+        if (i >= (uint32_t)kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        stage_info[s] = make_int4(rc, g, slot, s1 - s0);
+        const int e0 = s0 * P.seg_len;
+        const int e1 = min(P.vocab, s1 * P.seg_len);
         const uint32_t bytes = (uint32_t)(((e1 - e0 + 7) >> 3) << 4);
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(stages + (size_t)s * kStageBytes, P.logits + (size_t)row * P.ld + e0, bytes,
                  &full[s], pol);
+        ++i;
+      };
+      // Items blockIdx.x and G + blockIdx.x are static; later items come from the counter
+      // (numbered from 2G), with two claims in flight so the atomic's latency stays hidden
+      // behind the issue of two items.
+      const int b = blockIdx.x;
+      if (b < n_items) {
+        const bool dyn = 2 * G < n_items;
+        uint32_t p1 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
+        uint32_t p2 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
+        issue(b);
+        if (G + b < n_items) issue(G + b);
+        if (dyn) {
+          while (true) {
+            const int c1 = 2 * G + (int)p1;
+            if (c1 >= n_items) break;
+            p1 = atomicAdd(&P.ctrs[0], 1u);
+            issue(c1);
+            const int c2 = 2 * G + (int)p2;
+            if (c2 >= n_items) break;
+            p2 = atomicAdd(&P.ctrs[0], 1u);
+            issue(c2);
+          }
+        }
+      }
+      // end-of-work sentinels: one stage per consumer phase (every warpgroup sees one)
+      for (int c = 0; c < kWgStride; ++c, ++i) {
+        const int s = (int)(i % kStages);
+        if (c == 0) TL(14);
+        if (i >= (uint32_t)kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        stage_info[s] = make_int4(-1, 0, 0, 0);
+        mbar_arrive(&full[s]);
       }
     }
-    return;
+  } else {
+    // ---- consumers: warpgroup w reduces segment (w % kSegPerItem) of the stages with sequence
+    // number = w / kSegPerItem (mod kWgStride)
+    const int wg = (warp - 1) >> 2;
+    const int wq = (warp - 1) & 3;
+    const int jseg = wg % kSegPerItem;
+    bool first = true;
+    for (uint32_t i = wg / kSegPerItem;; i += kWgStride) {
+      const int s = (int)(i % kStages);
+      mbar_wait(&full[s], (i / kStages) & 1);
+      if (first && warp == 1 && lane == 0) TL(2);
+      first = false;
+      const int4 info = stage_info[s];
+      if (info.x < 0) break;
+      const int rc = info.x, g = info.y, slot = info.z, nsi = info.w;
+      if (jseg >= nsi) {  // short item (last group of a row): nothing for this warpgroup
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        continue;
+      }
+      const int seg = g * kSegPerItem + jseg;
+      const int e0 = seg * P.seg_len;
+      const int e1 = min(P.vocab, e0 + P.seg_len);
+      const int nchunks = (e1 - e0 + 7) >> 3;
+      const Partial pr = reduce_slice(stages + (size_t)s * kStageBytes + (size_t)jseg * P.seg_len * 2,
+                                      nchunks, e0, P.vocab, wq, lane, &empty[s]);
+      uint32_t done = 0;
+      if (lane == 0) {
+        ipart[slot * kPartPerItem + jseg * kWarpsPerSeg + wq] =
+            make_float4(pr.m, pr.s, __uint_as_float(pr.a), 0.f);
+        __threadfence_block();
+        done = (atomicAdd_block(&icnt[slot], 1u) + 1u == (uint32_t)(kWarpsPerSeg * nsi)) ? 1u : 0u;
+        if (done) {
+          // this warp completed the item: fold its warp partials (fixed order) -> group partial
+          __threadfence_block();
+          const float4* q = ipart + slot * kPartPerItem;
+          const FoldAcc f = fold_seq(kWarpsPerSeg * nsi, [&](int p) { return q[p]; });
+          P.gpart[(size_t)rc * n_grp + g] = make_float4(f.M, f.S, __uint_as_float(f.a), 0.f);
+          icnt[slot] = 0;
+          mbar_arrive(&slot_free[slot]);
+        }
+      }
+    }
+    if (lane == 0) TLMAX(3);
   }
-  // ---- consumers
-  const int wg = (warp - 1) >> 2;
-  const int wq = (warp - 1) & 3;
-  for (int i = wg; i < n_local; i += kConsumerWGs) {
-    const int s = i % kStages;
-    mbar_wait(&full[s], (i / kStages) & 1);
-    const long long u = u0 + i;
-    const int rc = (int)(u / n_seg);
-    const int seg = (int)(u - (long long)rc * n_seg);
-    const int row = row_list[rc];
-    const int e0 = seg * P.seg_len;
-    const int e1 = min(P.vocab, e0 + P.seg_len);
-    const int nchunks = (e1 - e0 + 7) >> 3;
-    const Partial pr = reduce_slice(stages + (size_t)s * kStageBytes, nchunks, e0, P.vocab, wq, lane);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
 
-    uint32_t last = 0;
-    if (lane == 0) {
-      P.partials[(size_t)row * n_part + seg * kWarpsPerSeg + wq] =
-          make_float4(pr.m, pr.s, __uint_as_float(pr.a), 0.f);
-      __threadfence();
-      last = (atomicAdd(&P.row_cnt[row], 1u) == (uint32_t)(n_part - 1)) ? 1u : 0u;
+  // CTA 0 publishes the compacted row list for the fold / tail kernel (K2, launched with PDL).
+  if (blockIdx.x == 0) {
+    for (int r = tid; r < n_masked; r += kThreads) P.row_list_out[r] = row_list[r];
+    if (tid == 0) P.ctrs[2] = (uint32_t)n_masked;
+  }
+  if (tid == 0) TL(4);
+}
+
+// ------------------------------------------------------------------ K2: fold + decisions
+// One CTA, launched programmatically dependent on K1: its launch and prologue overlap K1, and
+// griddepcontrol.wait returns once K1's writes are visible.  It folds every masked row's group
+// partials in fixed order (conf bits depend only on the row's bytes) and runs the tail.
+constexpr int kTailThreads = 512;
+constexpr size_t kTailSmemBytes = 96 * 1024;
+
+
+// Fold rows [r0, r0 + nr) of the compacted list from staged group partials; writes conf/argmax
+// (and the tail table when T != nullptr).
+__device__ __forceinline__ void fold_rows(const Params& P, const float4* gbuf, const uint16_t* rows,
+                                          int r0, int nr, TailSmem* T, int tid, int nthreads) {
+  const int n_grp = P.n_grp;
+  for (int r = tid; r < nr; r += nthreads) {
+    const float4* q = gbuf + r;  // group g of this row at q[g * nr]
+    DBGC(0);
+    FoldAcc f;
+    if (n_grp <= 16) {
+      float4 qr[16];
+#pragma unroll
+      for (int p = 0; p < 16; ++p) qr[p] = p < n_grp ? q[(size_t)p * nr] : make_float4(0.f, 0.f, 0.f, 0.f);
+      f = fold_tree16(n_grp, qr);
+    } else {
+      f = fold_seq(n_grp, [&](int p) { return q[(size_t)p * nr]; });
     }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) continue;
-    // ---- this warp completed row `row`: fold it
-    __threadfence();
-    float c;
-    int32_t a;
-    const bool bad = fold_row(P.partials + (size_t)row * n_part, n_part, lane, &c, &a);
-    uint32_t tail = 0;
-    if (lane == 0) {
-      P.conf[row] = c;
-      P.argmax[row] = a;
-      if (bad) atomicOr(P.dev_status, kDevNonfinite);
-      P.row_cnt[row] = 0;
-      if (P.mode != MODE_CONF) {
-        __threadfence();
-        tail = (atomicAdd(P.done_cnt, 1u) == (uint32_t)(n_masked - 1)) ? 1u : 0u;
-      }
+    DBGC(1);
+    const float c = __fdiv_rn(1.0f, f.S);
+    DBGC(2);
+    const int row = rows[r0 + r];
+    P.conf[row] = c;
+    P.argmax[row] = (int32_t)f.a;
+    DBGC(3);
+    if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
+    DBGC(4);
+    if (T) {
+      T->conf[row] = c;
+      T->amax[row] = (int32_t)f.a;
     }
-    tail = __shfl_sync(0xffffffffu, tail, 0);
-    if (!tail) continue;
-    if (P.mode == MODE_STEP) tail_step(P, keys + 64 * warp, lane);
-    if (P.mode == MODE_BP_LOCAL) tail_bp_local(P, lane);
-    if (lane == 0) *P.done_cnt = 0;
   }
 }
 
-constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 2 * kStages * 8 +
-                              2 * kMaxGroups * 4 + 16 + LOPA_MAX_ROWS * 2 + kWarps * 64 * 8;
+template <int MODE>
+__global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params P) {
+  extern __shared__ __align__(128) uint8_t tsm[];
+  TailSmem& T = *reinterpret_cast<TailSmem*>(tsm);
+  float4* gbuf = reinterpret_cast<float4*>(tsm + kTailBytes);
+  const int gcap = (int)((kTailSmemBytes - kTailBytes) / sizeof(float4));
+  const int tid = threadIdx.x;
+  const int W = P.window;
+  grid_dep_launch();
+  // Inputs not written by K1 (the branch tables, produced before K1 passed its own wait) are
+  // staged while K1 still runs; K1's outputs only after griddepcontrol.wait.
+  const int nb = max(0, min(*P.n_branches - P.branch_base, P.cap));
+  const int nt = nb * W;
+  const uint8_t* bmask = P.branch_mask + (size_t)P.branch_base * W;
+  const int32_t* btok = P.branch_tokens + (size_t)P.branch_base * W;
+  for (int idx = tid; idx < nt; idx += kTailThreads) {
+    T.msk[idx] = bmask[idx];
+    T.tok[idx] = btok[idx];
+    T.conf[idx] = 0.f;
+    T.amax[idx] = -1;
+  }
+  grid_dep_wait();
+  if (tid == 0) { TL(6); TLC(16); }
+#ifdef LOPA_TIMELINE
+  if (tid == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_timeline[21] = sm;
+  }
+#endif
+  const int n_masked = (int)P.ctrs[2];
+  const int n_grp = P.n_grp;
+  const int rows_per_batch = max(1, gcap / max(1, n_grp));
+  for (int rb = 0; rb < n_masked; rb += rows_per_batch) {
+    const int nr = min(rows_per_batch, n_masked - rb);
+    const float4* src = P.gpart + (size_t)rb * n_grp;
+    const int n = nr * n_grp;
+#pragma unroll 1
+    for (int base = 0; base < n; base += 8 * kTailThreads) {  // 8 loads in flight per thread
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {  // idx = g * nr + r (group-major: conflict-free reads later)
+        const int idx = base + u * kTailThreads + tid;
+        const int g = idx / nr, r = idx - g * nr;
+        if (idx < n) v[u] = __ldcg(src + (size_t)r * n_grp + g);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * kTailThreads + tid;
+        if (idx < n) gbuf[idx] = v[u];
+      }
+    }
+    if (tid == 0) TLC(17);
+    __syncthreads();
+    if (tid == 0) TL(10);
+    fold_rows(P, gbuf, P.row_list_out, rb, nr, &T, tid, kTailThreads);
+    if (tid == 0) TLC(18);
+
+    __syncthreads();
+    if (tid == 0) TL(15);
+  }
+  if (tid == 0) { TL(7); TLC(19); }
+  if (MODE == MODE_STEP) cta_tail_step<kTailThreads>(P, T, tid);
+  if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads>(P, T, tid);
+  if (tid == 0) {
+    P.ctrs[0] = 0;
+    TL(5);
+    TLC(20);
+  }
+}
+
+// MODE_CONF: rows folded by many CTAs (one thread per row), no decisions.
+__global__ void __launch_bounds__(256) lopa_fold_kernel(const Params P) {
+  grid_dep_launch();
+  grid_dep_wait();
+  const int n_masked = (int)P.ctrs[2];
+  const int n_grp = P.n_grp;
+  const int rc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rc < n_masked) {
+    const float4* q = P.gpart + (size_t)rc * n_grp;
+    const FoldAcc f = fold_seq(n_grp, [&](int p) { return __ldcg(q + p); });
+    const int row = P.row_list_out[rc];
+    P.conf[row] = __fdiv_rn(1.0f, f.S);
+    P.argmax[row] = (int32_t)f.a;
+    if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrs[0] = 0;
+}
+
+static_assert(kTailThreads >= 4 * LOPA_MAX_WINDOW, "rank uses 4 threads per position");
+static_assert(kTailBytes + 16 * 64 <= kTailSmemBytes, "tail scratch");
+constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + (2 * kStages + kItemSlots) * 8 +
+                              kStages * 16 + kItemSlots * kPartPerItem * 16 + kItemSlots * 4 +
+                              2 * kMaxGroups * 4 + 16 + LOPA_MAX_ROWS * 2;
 
 // ------------------------------------------------------------------ small decision kernels
 __global__ void anchor_kernel(const float* conf, const int32_t* argmax, const int32_t* tokens,
@@ -571,7 +988,12 @@ static int ensure_kernel_attrs(int device) {
     return LOPA_ERR_CUDA;
   if (major != 10 || minor != 0) return LOPA_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(lopa_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kSmemBytes) != cudaSuccess)
+                           (int)kSmemBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(lopa_tail_kernel<MODE_STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kTailSmemBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(lopa_tail_kernel<MODE_BP_LOCAL>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kTailSmemBytes) != cudaSuccess)
     return LOPA_ERR_CUDA;
   std::lock_guard<std::mutex> lk(g_mu);
   if (device >= 0 && device < 64) g_attr[device] = true;
@@ -599,32 +1021,61 @@ bool bind_device(void* stream, const void* ptr, int* device) {
   return true;
 }
 
+static size_t rowlist_bytes(int32_t max_rows) { return ((size_t)max_rows * 2 + 255) / 256 * 256; }
+
 size_t workspace_bytes(int32_t max_rows, int32_t vocab) {
   if (max_rows < 1 || vocab < 1) return 256;
   int32_t ns, sl;
   segmentation(vocab, &ns, &sl);
-  const size_t rc = (((size_t)max_rows * 4) + 255) / 256 * 256;
-  return 256 + rc + (size_t)max_rows * ns * kWarpsPerSeg * sizeof(float4);
+  return 256 + rowlist_bytes(max_rows) + (size_t)max_rows * num_groups(ns) * sizeof(float4);
 }
 
 bool carve_workspace(void* ws, size_t bytes, int32_t max_rows, int32_t vocab, Workspace* out) {
   if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255) != 0) return false;
   if (bytes < workspace_bytes(max_rows, vocab)) return false;
   uint8_t* p = static_cast<uint8_t*>(ws);
-  const size_t rc = (((size_t)max_rows * 4) + 255) / 256 * 256;
-  out->done_cnt = reinterpret_cast<uint32_t*>(p);
-  out->row_cnt = reinterpret_cast<uint32_t*>(p + 256);
-  out->partials = reinterpret_cast<float4*>(p + 256 + rc);
+  out->ctrs = reinterpret_cast<uint32_t*>(p);
+  out->row_list = reinterpret_cast<uint16_t*>(p + 256);
+  out->gpart = reinterpret_cast<float4*>(p + 256 + rowlist_bytes(max_rows));
   return true;
 }
 
+template <typename Kern>
+static cudaError_t launch_pdl(Kern kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              const Params& P) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, P);
+}
+
+// K1 (streaming reduction) then K2 (fold + decisions, or the fold only for MODE_CONF), both
+// with programmatic dependent launch so launch latency overlaps the previous kernel.
 static int launch_reduce(const Params& P, int device, cudaStream_t s) {
   int st = ensure_kernel_attrs(device);
   if (st != LOPA_OK) return st;
-  const int grid = num_sms(device);
+  // One SM is left to the fold/tail kernel: it becomes resident there while K1 streams (PDL)
+  // and, landing on the same SM step after step, runs with a warm instruction cache.
+  const int grid = LOPA_CTAS_PER_SM * num_sms(device) - (P.mode == MODE_CONF ? 0 : 1);
   if (grid <= 0) return LOPA_ERR_CUDA;
-  lopa_reduce_kernel<<<grid, kThreads, kSmemBytes, s>>>(P);
-  return cuda_status(cudaGetLastError());
+  cudaError_t e = launch_pdl(lopa_reduce_kernel, dim3(grid), dim3(kThreads), kSmemBytes, s, P);
+  if (e != cudaSuccess) return LOPA_ERR_CUDA;
+  if (P.mode == MODE_CONF) {
+    const int nb = (P.n_cand + 255) / 256;
+    e = launch_pdl(lopa_fold_kernel, dim3(nb), dim3(256), 0, s, P);
+  } else if (P.mode == MODE_STEP) {
+    e = launch_pdl(lopa_tail_kernel<MODE_STEP>, dim3(1), dim3(kTailThreads), kTailSmemBytes, s, P);
+  } else {
+    e = launch_pdl(lopa_tail_kernel<MODE_BP_LOCAL>, dim3(1), dim3(kTailThreads), kTailSmemBytes, s, P);
+  }
+  return cuda_status(e);
 }
 
 static bool logits_ok(const void* logits, int64_t ld, int32_t vocab) {
@@ -656,14 +1107,15 @@ static Params base_params(const lopa_step_args_t* a, const Workspace& ws) {
   P.ld = a->ld;
   P.vocab = a->vocab;
   segmentation(a->vocab, &P.n_seg, &P.seg_len);
+  P.n_grp = num_groups(P.n_seg);
   P.window = a->window;
   P.n_branches = a->n_branches;
   P.conf = a->conf;
   P.argmax = a->argmax;
   P.dev_status = a->dev_status;
-  P.done_cnt = ws.done_cnt;
-  P.row_cnt = ws.row_cnt;
-  P.partials = ws.partials;
+  P.ctrs = ws.ctrs;
+  P.row_list_out = ws.row_list;
+  P.gpart = ws.gpart;
   P.branch_tokens = a->branch_tokens;
   P.branch_mask = a->branch_mask;
   P.k = a->k;
@@ -724,6 +1176,25 @@ using namespace lopa;
 
 extern "C" int lopa_version(void) { return LOPA_VERSION; }
 
+// Debug: copy the per-CTA phase timeline of the last launch (timeline builds only; returns the
+// number of slots per CTA, 0 if the build has no timeline).
+extern "C" int lopa_debug_timeline(unsigned long long* out, int n_ctas) {
+#ifdef LOPA_TIMELINE
+  if (!out || n_ctas < 1 || n_ctas > 256) return 0;
+  cudaDeviceSynchronize();
+  {
+    long long d[8];
+    cudaMemcpyFromSymbol(d, lopa::g_dbg, sizeof(d));
+    fprintf(stderr, "fold clk: load+tree %lld fdiv %lld stores %lld status %lld\n", d[1] - d[0], d[2] - d[1], d[3] - d[2], d[4] - d[3]);
+  }
+  if (cudaMemcpyFromSymbol(out, lopa::g_timeline, sizeof(unsigned long long) * n_ctas * lopa::kTlSlots) != cudaSuccess) return 0;
+  return lopa::kTlSlots;
+#else
+  (void)out; (void)n_ctas;
+  return 0;
+#endif
+}
+
 extern "C" const char* lopa_status_string(int status) {
   switch (status) {
     case LOPA_OK: return "ok";
@@ -766,15 +1237,16 @@ extern "C" int lopa_confidence(const void* logits, int64_t ld, int32_t n_rows, i
   P.ld = ld;
   P.vocab = vocab;
   segmentation(vocab, &P.n_seg, &P.seg_len);
+  P.n_grp = num_groups(P.n_seg);
   P.n_cand = n_rows;
   P.row_mask = row_mask;
   P.window = 1;
   P.conf = conf;
   P.argmax = argmax;
   P.dev_status = dev_status;
-  P.done_cnt = ws.done_cnt;
-  P.row_cnt = ws.row_cnt;
-  P.partials = ws.partials;
+  P.ctrs = ws.ctrs;
+  P.row_list_out = ws.row_list;
+  P.gpart = ws.gpart;
   P.mode = MODE_CONF;
   return launch_reduce(P, dev, s);
 }

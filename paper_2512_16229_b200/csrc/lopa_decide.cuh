@@ -29,7 +29,8 @@ __device__ __forceinline__ uint32_t ordered_bits(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// Load the window row of branch state (tok/msk) and conf/argmax (L2-coherent).
+// Load the window row of branch state (tok/msk) and conf/argmax.  conf / msk may point to shared
+// memory (generic loads); amax is global and read L2-coherently (written by other CTAs).
 __device__ __forceinline__ void load_window(WinRegs& r, const float* conf, const int32_t* amax,
                                             const int32_t* tok, const uint8_t* msk, int W,
                                             int lane) {
@@ -39,7 +40,7 @@ __device__ __forceinline__ void load_window(WinRegs& r, const float* conf, const
     const bool in = i < W;
     r.msk[s] = in ? (uint32_t)(msk[i] != 0) : 0u;
     r.tok[s] = in ? tok[i] : 0;
-    r.conf[s] = (in && r.msk[s]) ? __ldcg(conf + i) : 0.f;
+    r.conf[s] = (in && r.msk[s]) ? conf[i] : 0.f;
     r.amax[s] = (in && r.msk[s]) ? __ldcg(amax + i) : -1;
   }
 }
@@ -47,6 +48,7 @@ __device__ __forceinline__ void load_window(WinRegs& r, const float* conf, const
 // Eq. 2: lane j < n_br scores branch j: sum of conf over its masked positions in
 // position order (fp64), divided by the count, rounded once to fp32; 1.0 if none (R8).
 // Absent branches (n_br <= j < max_br) score -inf.  Returns the branch's score in lane j.
+// conf / mask are generic pointers (shared memory in the fused tail).
 __device__ __forceinline__ float warp_branch_score(const float* conf, const uint8_t* mask,
                                                    int n_br, int max_br, int W, int lane) {
   float score = -INFINITY;
@@ -57,7 +59,7 @@ __device__ __forceinline__ float warp_branch_score(const float* conf, const uint
     int cnt = 0;
     for (int i = 0; i < W; ++i) {
       if (m[i]) {
-        sum += (double)__ldcg(c + i);
+        sum += (double)c[i];
         ++cnt;
       }
     }
@@ -140,6 +142,9 @@ __device__ __forceinline__ void warp_spawn(const WinRegs& b0, int W, int k, uint
     rank[s] = b0.msk[s] ? cnt : 1 << 20;
   }
   __syncwarp();
+#ifdef TL
+  if (lane == 0) TL(12);
+#endif
   // Branch j (1..n) fills p_j = the position of rank j - 1.
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
@@ -160,6 +165,9 @@ __device__ __forceinline__ void warp_spawn(const WinRegs& b0, int W, int k, uint
     }
   }
   if (lane == 0) *n_branches = n + 1;
+#ifdef TL
+  if (lane == 0) TL(13);
+#endif
 }
 
 // Store the window registers to a table row.

@@ -9,19 +9,31 @@ namespace lopa {
 
 // Canonical segmentation of a row: n_seg = ceil(V / 8192) segments of
 // seg_len = 8 * ceil(ceil(V / n_seg) / 8) elements (the last one shorter).  Depends on V only.
+#ifndef LOPA_SEG_ELEMS
+#define LOPA_SEG_ELEMS 8192
+#endif
+constexpr int kSegElems = LOPA_SEG_ELEMS;          // max elements per canonical segment
+constexpr int kChunksPerLane = kSegElems / 8 / 128;  // 16-byte chunks per lane per segment
+
 inline void segmentation(int32_t vocab, int32_t* n_seg, int32_t* seg_len) {
-  const int32_t ns = (vocab + 8191) / 8192;
+  const int32_t ns = (vocab + kSegElems - 1) / kSegElems;
   const int32_t per = (vocab + ns - 1) / ns;
   *n_seg = ns;
   *seg_len = ((per + 7) / 8) * 8;
 }
 
-constexpr int kWarpsPerSeg = 4;  // partials per segment (one per consumer warp)
+constexpr int kWarpsPerSeg = 4;  // warp partials per segment (one per consumer warp)
+#ifndef LOPA_SEG_PER_ITEM
+#define LOPA_SEG_PER_ITEM 2
+#endif
+constexpr int kSegPerItem = LOPA_SEG_PER_ITEM;  // canonical group = work item = one TMA copy
+
+inline int32_t num_groups(int32_t n_seg) { return (n_seg + kSegPerItem - 1) / kSegPerItem; }
 
 struct Workspace {
-  uint32_t* done_cnt;   // [1]
-  uint32_t* row_cnt;    // [max_rows]
-  float4* partials;     // [max_rows][n_seg * 4]
+  uint32_t* ctrs;       // [0] work-item counter (zero between calls), [2] n_masked
+  uint16_t* row_list;   // [max_rows] compacted masked-row list
+  float4* gpart;        // [max_rows][n_groups] group partials
 };
 
 size_t workspace_bytes(int32_t max_rows, int32_t vocab);

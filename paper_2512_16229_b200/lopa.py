@@ -17,6 +17,8 @@ import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "liblopa.so")
+if os.environ.get("LOPA_LIB_VARIANT"):   # tuning builds (paper_2512_16229_b200/build.py --variant)
+    LIB_PATH = os.path.join(_PKG, f"liblopa_{os.environ['LOPA_LIB_VARIANT']}.so")
 
 LOPA_OK = 0
 DEV_EMPTY_MASK = 1
@@ -73,6 +75,7 @@ _SIGS = {
     "lopa_bp_step": (_i32, [_c_void_p, ctypes.POINTER(StepArgs), _i32, _c_void_p, _c_void_p]),
     "lopa_bp_check": (_i32, [_c_void_p]),
     "lopa_bp_destroy": (None, [_c_void_p]),
+    "lopa_debug_timeline": (_i32, [_c_void_p, _i32]),
     "lopa_syn_generate": (_i32, [_u64, _i32, _i32, _i64, _i32, _i32, _c_void_p, _c_void_p, _i32,
                                  _c_void_p, _c_void_p]),
 }

@@ -49,22 +49,11 @@ def decision_gaps(conf_w, mask_w, anchor_mask, k, tau, scores):
     return gaps
 
 
-def oracle_decisions_on(conf, argmax, tok, msk, n_br, k, tau):
-    """The oracle's a2-a4 decisions recomputed on given (GPU fp32) conf values."""
-    scores = [O.branch_score(conf[j], msk[j]) for j in range(n_br)]
-    w = O.verify_select(scores)
-    if not np.asarray(msk[w]).any():
-        return scores, w, None, None
-    anc = O.anchor_fill(conf[w], argmax[w], tok[w], msk[w], tau)
-    sp = O.spawn_branches(conf[w], argmax[w], anc.tokens, anc.mask, k)
-    return scores, w, anc, sp
-
-
-def check_step(out, logits_u16, tok, msk, n_br, k, tau, exempt_counter=None):
+def check_step(out, logits_u16, tok, msk, n_br, k, tau, exempt_counter=None, vocab=None):
     """Compare one fused-step output with the oracle on the same inputs.  Returns the oracle
     StepResult.  tok/msk: numpy [max_br][W]; logits_u16: numpy [>=n_br][W][ld]."""
     W = msk.shape[1]
-    V_rows = logits_u16[:n_br]
+    V_rows = logits_u16[:n_br, :, :vocab] if vocab else logits_u16[:n_br]   # the oracle reads V entries, not ld
     ref = O.step(V_rows, tok[:n_br], msk[:n_br], k, tau)
     g_conf = out.conf.cpu().numpy()[:n_br].astype(np.float64)
     g_amax = out.argmax.cpu().numpy()[:n_br].astype(np.int64)
@@ -84,7 +73,7 @@ def check_step(out, logits_u16, tok, msk, n_br, k, tau, exempt_counter=None):
     # a2: scores within tolerance
     assert np.max(np.abs(g_scores - np.array(ref.scores)), initial=0.0) <= CONF_TOL
     # decisions: exactly the oracle's decisions on the GPU's own fp32 values
-    cs, cw, canc, csp = oracle_decisions_on(np.where(sel, g_conf, np.nan), g_amax, tok, msk, n_br, k, tau)
+    cs = [O.branch_score(np.where(sel, g_conf, np.nan)[j], msk[j]) for j in range(n_br)]
     # fp32-rounded score ties -> lowest index (the GPU selects on its fp32 scores)
     gs32 = [float(np.float32(x)) for x in cs]
     assert g_w == O.verify_select(gs32)

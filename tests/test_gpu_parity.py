@@ -244,7 +244,7 @@ def _run_steps(L, seed, V, W, k, tau, iters, extras, blk=0, counter=None):
         L.syn_generate(seed, blk, V, tok, msk, n_branches=n, extras=extras, out=logits[:n])
         out = st.step(logits, nb, tok, msk)
         torch.cuda.synchronize()
-        G.check_step(out, G.to_np_u16(logits), tok.cpu().numpy(), msk.cpu().numpy(), n, k, tau, counter)
+        G.check_step(out, G.to_np_u16(logits), tok.cpu().numpy(), msk.cpu().numpy(), n, k, tau, counter, vocab=V)
         if int(out.n_next.item()) == 0:
             return it + 1
         tok, msk, nb = out.next_tokens.clone(), out.next_mask.clone(), out.n_next.clone()
