@@ -46,14 +46,12 @@ __device__ __forceinline__ void tl_max(int slot) {
 }
 #define TLMAX(slot) tl_max(slot)
 __device__ __forceinline__ void tl_clk(int slot) { g_timeline[blockIdx.x * kTlSlots + slot] = clock64(); }
-__device__ long long g_dbg[8];
-#define DBGC(k) do { if (threadIdx.x == 0) g_dbg[k] = clock64(); } while (0)
+
 #define TLC(slot) tl_clk(slot)
 #else
 #define TL(slot) ((void)0)
 #define TLMAX(slot) ((void)0)
 #define TLC(slot) ((void)0)
-#define DBGC(k) ((void)0)
 #endif
 }  // namespace lopa
 #include "lopa_decide.cuh"
@@ -100,7 +98,6 @@ struct Params {
   int32_t* argmax;
   int32_t* dev_status;
   uint32_t* ctrs;              // [0] work-item counter, [2] n_masked (K1 -> K2)
-  uint16_t* row_list_out;      // [n_cand] compacted row list (K1 -> K2)
   float4* gpart;               // [n_cand][n_grp] group partials (m, s, argmax bits, -)
   int mode;
   // tails
@@ -709,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
           __threadfence_block();
           const float4* q = ipart + slot * kPartPerItem;
           const FoldAcc f = fold_seq(kWarpsPerSeg * nsi, [&](int p) { return q[p]; });
-          P.gpart[(size_t)rc * n_grp + g] = make_float4(f.M, f.S, __uint_as_float(f.a), 0.f);
+          P.gpart[(size_t)row_list[rc] * n_grp + g] = make_float4(f.M, f.S, __uint_as_float(f.a), 0.f);
           icnt[slot] = 0;
           mbar_arrive(&slot_free[slot]);
         }
@@ -718,11 +715,6 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     if (lane == 0) TLMAX(3);
   }
 
-  // CTA 0 publishes the compacted row list for the fold / tail kernel (K2, launched with PDL).
-  if (blockIdx.x == 0) {
-    for (int r = tid; r < n_masked; r += kThreads) P.row_list_out[r] = row_list[r];
-    if (tid == 0) P.ctrs[2] = (uint32_t)n_masked;
-  }
   if (tid == 0) TL(4);
 }
 
@@ -731,103 +723,94 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
 // griddepcontrol.wait returns once K1's writes are visible.  It folds every masked row's group
 // partials in fixed order (conf bits depend only on the row's bytes) and runs the tail.
 constexpr int kTailThreads = 512;
-constexpr size_t kTailSmemBytes = 96 * 1024;
+constexpr size_t kTailSmemBytes = kTailBytes + LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW * 2;
 
 
-// Fold rows [r0, r0 + nr) of the compacted list from staged group partials; writes conf/argmax
-// (and the tail table when T != nullptr).
-__device__ __forceinline__ void fold_rows(const Params& P, const float4* gbuf, const uint16_t* rows,
-                                          int r0, int nr, TailSmem* T, int tid, int nthreads) {
-  const int n_grp = P.n_grp;
-  for (int r = tid; r < nr; r += nthreads) {
-    const float4* q = gbuf + r;  // group g of this row at q[g * nr]
-    DBGC(0);
-    FoldAcc f;
-    if (n_grp <= 16) {
-      float4 qr[16];
+// Fold one row's group partials (read straight from the workspace, all loads in flight) ->
+// conf, argmax.  Fixed order: the 16-slot pairwise tree for n_grp <= 16, sequential beyond.
+__device__ __forceinline__ FoldAcc fold_row_global(const float4* q, int n_grp) {
+  if (n_grp <= 16) {
+    float4 qr[16];
 #pragma unroll
-      for (int p = 0; p < 16; ++p) qr[p] = p < n_grp ? q[(size_t)p * nr] : make_float4(0.f, 0.f, 0.f, 0.f);
-      f = fold_tree16(n_grp, qr);
-    } else {
-      f = fold_seq(n_grp, [&](int p) { return q[(size_t)p * nr]; });
-    }
-    DBGC(1);
-    const float c = __fdiv_rn(1.0f, f.S);
-    DBGC(2);
-    const int row = rows[r0 + r];
-    P.conf[row] = c;
-    P.argmax[row] = (int32_t)f.a;
-    DBGC(3);
-    if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
-    DBGC(4);
-    if (T) {
-      T->conf[row] = c;
-      T->amax[row] = (int32_t)f.a;
-    }
+    for (int p = 0; p < 16; ++p) qr[p] = p < n_grp ? __ldcg(q + p) : make_float4(0.f, 0.f, 0.f, 0.f);
+    return fold_tree16(n_grp, qr);
   }
+  return fold_seq(n_grp, [&](int p) { return __ldcg(q + p); });
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params P) {
   extern __shared__ __align__(128) uint8_t tsm[];
   TailSmem& T = *reinterpret_cast<TailSmem*>(tsm);
-  float4* gbuf = reinterpret_cast<float4*>(tsm + kTailBytes);
-  const int gcap = (int)((kTailSmemBytes - kTailBytes) / sizeof(float4));
-  const int tid = threadIdx.x;
+  uint16_t* rows = reinterpret_cast<uint16_t*>(tsm + kTailBytes);  // masked rows, ascending
+  __shared__ uint32_t s_wcnt[kTailThreads / 32 + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
   grid_dep_launch();
-  // Inputs not written by K1 (the branch tables, produced before K1 passed its own wait) are
-  // staged while K1 still runs; K1's outputs only after griddepcontrol.wait.
+  // Inputs are not written by K1 (the tables were produced before K1 passed its own wait), so
+  // they are staged, and the masked-row list built, while K1 still streams.
   const int nb = max(0, min(*P.n_branches - P.branch_base, P.cap));
-  const int nt = nb * W;
+  const int nt = nb * W;  // <= LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW = 2048
   const uint8_t* bmask = P.branch_mask + (size_t)P.branch_base * W;
   const int32_t* btok = P.branch_tokens + (size_t)P.branch_base * W;
-  for (int idx = tid; idx < nt; idx += kTailThreads) {
-    T.msk[idx] = bmask[idx];
-    T.tok[idx] = btok[idx];
-    T.conf[idx] = 0.f;
-    T.amax[idx] = -1;
-  }
-  grid_dep_wait();
-  if (tid == 0) { TL(6); TLC(16); }
-#ifdef LOPA_TIMELINE
-  if (tid == 0) {
-    unsigned sm;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    g_timeline[21] = sm;
-  }
-#endif
-  const int n_masked = (int)P.ctrs[2];
-  const int n_grp = P.n_grp;
-  const int rows_per_batch = max(1, gcap / max(1, n_grp));
-  for (int rb = 0; rb < n_masked; rb += rows_per_batch) {
-    const int nr = min(rows_per_batch, n_masked - rb);
-    const float4* src = P.gpart + (size_t)rb * n_grp;
-    const int n = nr * n_grp;
-#pragma unroll 1
-    for (int base = 0; base < n; base += 8 * kTailThreads) {  // 8 loads in flight per thread
-      float4 v[8];
+  uint32_t mine[4];  // thread owns rows 4 tid .. 4 tid + 3 (contiguous: ascending order)
+  int cnt = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {  // idx = g * nr + r (group-major: conflict-free reads later)
-        const int idx = base + u * kTailThreads + tid;
-        const int g = idx / nr, r = idx - g * nr;
-        if (idx < n) v[u] = __ldcg(src + (size_t)r * n_grp + g);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = base + u * kTailThreads + tid;
-        if (idx < n) gbuf[idx] = v[u];
-      }
+  for (int u = 0; u < 4; ++u) {
+    const int idx = 4 * tid + u;
+    const uint8_t mk = idx < nt ? bmask[idx] : (uint8_t)0;
+    if (idx < nt) {
+      T.msk[idx] = mk;
+      T.tok[idx] = btok[idx];
+      T.conf[idx] = 0.f;
+      T.amax[idx] = -1;
     }
-    if (tid == 0) TLC(17);
-    __syncthreads();
-    if (tid == 0) TL(10);
-    fold_rows(P, gbuf, P.row_list_out, rb, nr, &T, tid, kTailThreads);
-    if (tid == 0) TLC(18);
-
-    __syncthreads();
-    if (tid == 0) TL(15);
+    mine[u] = mk ? 1u : 0u;
+    cnt += mk ? 1 : 0;
   }
+  // block-wide exclusive scan of the per-thread masked counts -> compacted row list
+  int incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) s_wcnt[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int v = lane < kTailThreads / 32 ? (int)s_wcnt[lane] : 0;
+    int x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane < kTailThreads / 32) s_wcnt[lane] = x - v;  // exclusive warp offsets
+    if (lane == kTailThreads / 32 - 1) s_wcnt[kTailThreads / 32] = x;
+  }
+  __syncthreads();
+  {
+    int pos = (int)s_wcnt[warp] + incl - cnt;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (mine[u]) rows[pos++] = (uint16_t)(4 * tid + u);
+  }
+  const int n_masked = (int)s_wcnt[kTailThreads / 32];
+  __syncthreads();
+  grid_dep_wait();  // K1's group partials are visible from here on
+  if (tid == 0) { TL(6); TLC(16); }
+  const int n_grp = P.n_grp;
+  for (int rc = tid; rc < n_masked; rc += kTailThreads) {
+    const int row = rows[rc];
+    const FoldAcc f = fold_row_global(P.gpart + (size_t)row * n_grp, n_grp);
+    const float c = __fdiv_rn(1.0f, f.S);
+    P.conf[row] = c;
+    P.argmax[row] = (int32_t)f.a;
+    if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
+    T.conf[row] = c;
+    T.amax[row] = (int32_t)f.a;
+  }
+  __syncthreads();
   if (tid == 0) { TL(7); TLC(19); }
   if (MODE == MODE_STEP) cta_tail_step<kTailThreads>(P, T, tid);
   if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads>(P, T, tid);
@@ -838,26 +821,24 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   }
 }
 
-// MODE_CONF: rows folded by many CTAs (one thread per row), no decisions.
+// MODE_CONF: one thread per candidate row, no decisions.
 __global__ void __launch_bounds__(256) lopa_fold_kernel(const Params P) {
   grid_dep_launch();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = r < P.n_cand && (P.row_mask == nullptr || P.row_mask[r] != 0);
   grid_dep_wait();
-  const int n_masked = (int)P.ctrs[2];
-  const int n_grp = P.n_grp;
-  const int rc = blockIdx.x * blockDim.x + threadIdx.x;
-  if (rc < n_masked) {
-    const float4* q = P.gpart + (size_t)rc * n_grp;
-    const FoldAcc f = fold_seq(n_grp, [&](int p) { return __ldcg(q + p); });
-    const int row = P.row_list_out[rc];
-    P.conf[row] = __fdiv_rn(1.0f, f.S);
-    P.argmax[row] = (int32_t)f.a;
+  if (valid) {
+    const FoldAcc f = fold_row_global(P.gpart + (size_t)r * P.n_grp, P.n_grp);
+    P.conf[r] = __fdiv_rn(1.0f, f.S);
+    P.argmax[r] = (int32_t)f.a;
     if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrs[0] = 0;
 }
 
 static_assert(kTailThreads >= 4 * LOPA_MAX_WINDOW, "rank uses 4 threads per position");
-static_assert(kTailBytes + 16 * 64 <= kTailSmemBytes, "tail scratch");
+static_assert(4 * kTailThreads >= LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW, "4 table rows per thread");
+
 constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + (2 * kStages + kItemSlots) * 8 +
                               kStages * 16 + kItemSlots * kPartPerItem * 16 + kItemSlots * 4 +
                               2 * kMaxGroups * 4 + 16 + LOPA_MAX_ROWS * 2;
@@ -1021,13 +1002,11 @@ bool bind_device(void* stream, const void* ptr, int* device) {
   return true;
 }
 
-static size_t rowlist_bytes(int32_t max_rows) { return ((size_t)max_rows * 2 + 255) / 256 * 256; }
-
 size_t workspace_bytes(int32_t max_rows, int32_t vocab) {
   if (max_rows < 1 || vocab < 1) return 256;
   int32_t ns, sl;
   segmentation(vocab, &ns, &sl);
-  return 256 + rowlist_bytes(max_rows) + (size_t)max_rows * num_groups(ns) * sizeof(float4);
+  return 256 + (size_t)max_rows * num_groups(ns) * sizeof(float4);
 }
 
 bool carve_workspace(void* ws, size_t bytes, int32_t max_rows, int32_t vocab, Workspace* out) {
@@ -1035,8 +1014,7 @@ bool carve_workspace(void* ws, size_t bytes, int32_t max_rows, int32_t vocab, Wo
   if (bytes < workspace_bytes(max_rows, vocab)) return false;
   uint8_t* p = static_cast<uint8_t*>(ws);
   out->ctrs = reinterpret_cast<uint32_t*>(p);
-  out->row_list = reinterpret_cast<uint16_t*>(p + 256);
-  out->gpart = reinterpret_cast<float4*>(p + 256 + rowlist_bytes(max_rows));
+  out->gpart = reinterpret_cast<float4*>(p + 256);
   return true;
 }
 
@@ -1050,7 +1028,11 @@ static cudaError_t launch_pdl(Kern kernel, dim3 grid, dim3 block, size_t smem, c
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+#ifdef LOPA_NO_PDL
+  attr[0].val.programmaticStreamSerializationAllowed = 0;
+#else
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+#endif
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, P);
@@ -1114,7 +1096,6 @@ static Params base_params(const lopa_step_args_t* a, const Workspace& ws) {
   P.argmax = a->argmax;
   P.dev_status = a->dev_status;
   P.ctrs = ws.ctrs;
-  P.row_list_out = ws.row_list;
   P.gpart = ws.gpart;
   P.branch_tokens = a->branch_tokens;
   P.branch_mask = a->branch_mask;
@@ -1182,11 +1163,7 @@ extern "C" int lopa_debug_timeline(unsigned long long* out, int n_ctas) {
 #ifdef LOPA_TIMELINE
   if (!out || n_ctas < 1 || n_ctas > 256) return 0;
   cudaDeviceSynchronize();
-  {
-    long long d[8];
-    cudaMemcpyFromSymbol(d, lopa::g_dbg, sizeof(d));
-    fprintf(stderr, "fold clk: load+tree %lld fdiv %lld stores %lld status %lld\n", d[1] - d[0], d[2] - d[1], d[3] - d[2], d[4] - d[3]);
-  }
+
   if (cudaMemcpyFromSymbol(out, lopa::g_timeline, sizeof(unsigned long long) * n_ctas * lopa::kTlSlots) != cudaSuccess) return 0;
   return lopa::kTlSlots;
 #else
@@ -1245,7 +1222,6 @@ extern "C" int lopa_confidence(const void* logits, int64_t ld, int32_t n_rows, i
   P.argmax = argmax;
   P.dev_status = dev_status;
   P.ctrs = ws.ctrs;
-  P.row_list_out = ws.row_list;
   P.gpart = ws.gpart;
   P.mode = MODE_CONF;
   return launch_reduce(P, dev, s);

@@ -31,9 +31,8 @@ constexpr int kSegPerItem = LOPA_SEG_PER_ITEM;  // canonical group = work item =
 inline int32_t num_groups(int32_t n_seg) { return (n_seg + kSegPerItem - 1) / kSegPerItem; }
 
 struct Workspace {
-  uint32_t* ctrs;       // [0] work-item counter (zero between calls), [2] n_masked
-  uint16_t* row_list;   // [max_rows] compacted masked-row list
-  float4* gpart;        // [max_rows][n_groups] group partials
+  uint32_t* ctrs;       // [0] work-item counter (zero between calls)
+  float4* gpart;        // [max_rows][n_groups] group partials, indexed by raw row
 };
 
 size_t workspace_bytes(int32_t max_rows, int32_t vocab);

@@ -35,3 +35,22 @@ order = np.argsort(lu)
 print("last_unit percentiles", np.percentile(lu, [0, 10, 25, 50, 75, 90, 95, 100]).round(2))
 print("slowest CTAs (block, last_unit, first_data):", [(int(b), round(float(lu[b]), 2), round(float(rel[b, 2]), 2)) for b in order[-16:]])
 print("fastest CTAs:", [(int(b), round(float(lu[b]), 2)) for b in order[:8]])
+# K2 alone, back to back (warm): event timing
+import ctypes as C
+L = lopa.lib()
+if hasattr(L, "lopa_debug_tail_only"):
+    f = L.lopa_debug_tail_only
+    f.argtypes = [C.POINTER(lopa.StepArgs), C.c_void_p]
+    a = st.args(bufs[0], nb, tok, msk)
+    sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for _ in range(10): f(C.byref(a), sp)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(200): f(C.byref(a), sp)
+    e1.record(); torch.cuda.synchronize()
+    print("K2 alone back-to-back: %.2f us/launch" % (e0.elapsed_time(e1) * 1000 / 200))
+    e0.record()
+    for _ in range(200): st.step(bufs[0], nb, tok, msk, validate=False)
+    e1.record(); torch.cuda.synchronize()
+    print("full step same buffer (L2-warm logits) back-to-back: %.2f us/step" % (e0.elapsed_time(e1) * 1000 / 200))
