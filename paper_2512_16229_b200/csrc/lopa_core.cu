@@ -312,8 +312,9 @@ __device__ __forceinline__ Partial reduce_slice(const uint8_t* stage, int nchunk
 
 // ------------------------------------------------------------------ canonical folds
 // Fold of partials q[0..n) in index order: M = max m; S = sum_p s_p * 2^((m_p - M) log2 e) in p
-// order; argmax = the smallest index among partials with m_p = M.  A partial whose max is -inf
-// contributes 0 (or NaN if it saw a NaN); a fold whose max is -inf has S = 0 (or NaN).
+// order; argmax = the smallest index among partials with m_p = M.  A partial with m = -inf
+// contributes s * 0 = 0 (NaN if it saw a NaN); when M = -inf (every element -inf) the factor is 1,
+// so S = sum s = 0 (or NaN) and a row fold reports it as non-finite (R20).
 struct FoldAcc {
   float M, S;
   uint32_t a;
@@ -327,12 +328,8 @@ __device__ __forceinline__ FoldAcc fold_seq(int n, Get get) {
 #pragma unroll 1
   for (int p = 0; p < n; ++p) {
     const float4 q = get(p);
-    if (q.x == -INFINITY || M == -INFINITY) {
-      r.S += isnan(q.y) ? q.y : 0.f;
-    } else {
-      r.S += q.y * ex2((q.x - M) * kLog2e);
-      if (q.x == M) r.a = min(r.a, __float_as_uint(q.z));
-    }
+    r.S += q.y * (M == -INFINITY ? 1.f : ex2((q.x - M) * kLog2e));
+    if (q.x == M) r.a = min(r.a, __float_as_uint(q.z));
   }
   return r;
 }
@@ -343,21 +340,13 @@ __device__ __forceinline__ FoldAcc fold_seq(int n, Get get) {
 __device__ __forceinline__ FoldAcc fold_tree16(int n, const float4 (&q)[16]) {
   float M = -INFINITY;
 #pragma unroll
-  for (int p = 0; p < 16; ++p)
-    if (p < n) M = fmaxf(M, q[p].x);
+  for (int p = 0; p < 16; ++p) M = fmaxf(M, p < n ? q[p].x : -INFINITY);
   float t[16];
   uint32_t a = 0xFFFFFFFFu;
 #pragma unroll
   for (int p = 0; p < 16; ++p) {
-    t[p] = 0.f;
-    if (p < n) {
-      if (q[p].x == -INFINITY || M == -INFINITY) {
-        t[p] = isnan(q[p].y) ? q[p].y : 0.f;
-      } else {
-        t[p] = q[p].y * ex2((q[p].x - M) * kLog2e);
-        if (q[p].x == M) a = min(a, __float_as_uint(q[p].z));
-      }
-    }
+    t[p] = p < n ? q[p].y * (M == -INFINITY ? 1.f : ex2((q[p].x - M) * kLog2e)) : 0.f;
+    a = (p < n && q[p].x == M) ? min(a, __float_as_uint(q[p].z)) : a;
   }
 #pragma unroll
   for (int w = 8; w >= 1; w >>= 1)
