@@ -203,6 +203,13 @@ int lopa_bp_step(lopa_bp_t* bp, const lopa_step_args_t* args, int32_t b_loc, voi
 int lopa_bp_check(lopa_bp_t* bp);
 void lopa_bp_destroy(lopa_bp_t* bp);
 
+/* Measurement: record a CUDA event pair around every K1 (vocabulary-reduction kernel) launch of
+ * the next max_records lopa_step / lopa_confidence / lopa_bp_local calls (events recorded on the
+ * call's stream).  lopa_profile_read synchronises, writes up to max durations in ms and the
+ * count, and disables recording.  Errors: INVALID_ARG, CUDA. */
+int lopa_profile_enable(int32_t max_records);
+int lopa_profile_read(float* k1_ms, int32_t max, int32_t* n_out);
+
 /* Debug: per-CTA phase timeline (%globaltimer ns) of the last reduction launch, for builds
  * compiled with -DLOPA_TIMELINE; returns the slots per CTA written to out[n_ctas][slots], or 0.
  * Slots: 0 CTA start, 1 producer start, 2 first stage consumed, 3 last unit consumed,

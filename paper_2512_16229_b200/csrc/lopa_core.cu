@@ -21,6 +21,7 @@
 //     (conf bits depend only on the row's bytes), then runs the tail with all its threads:
 //     Eq. 2 scores + select, Eq. 1 anchor, top-k spawn (MODE_STEP) or the local branch-parallel
 //     record (MODE_BP_LOCAL).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -1027,6 +1028,24 @@ static cudaError_t launch_pdl(Kern kernel, dim3 grid, dim3 block, size_t smem, c
   return cudaLaunchKernelEx(&cfg, kernel, P);
 }
 
+// Optional K1 timing (lopa_profile_enable / lopa_profile_read).
+struct Profiler {
+  std::mutex mu;
+  int cap = 0, n = 0;
+  cudaEvent_t* ev = nullptr;  // [cap][2]
+};
+static Profiler g_prof;
+
+static void prof_record(int which, cudaStream_t s, int* slot) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  if (!g_prof.ev) return;
+  if (which == 0) {
+    if (g_prof.n >= g_prof.cap) { *slot = -1; return; }
+    *slot = g_prof.n++;
+  }
+  if (*slot >= 0) cudaEventRecord(g_prof.ev[2 * *slot + which], s);
+}
+
 // K1 (streaming reduction) then K2 (fold + decisions, or the fold only for MODE_CONF), both
 // with programmatic dependent launch so launch latency overlaps the previous kernel.
 static int launch_reduce(const Params& P, int device, cudaStream_t s) {
@@ -1036,8 +1055,11 @@ static int launch_reduce(const Params& P, int device, cudaStream_t s) {
   // and, landing on the same SM step after step, runs with a warm instruction cache.
   const int grid = LOPA_CTAS_PER_SM * num_sms(device) - (P.mode == MODE_CONF ? 0 : 1);
   if (grid <= 0) return LOPA_ERR_CUDA;
+  int pslot = -1;
+  prof_record(0, s, &pslot);
   cudaError_t e = launch_pdl(lopa_reduce_kernel, dim3(grid), dim3(kThreads), kSmemBytes, s, P);
   if (e != cudaSuccess) return LOPA_ERR_CUDA;
+  prof_record(1, s, &pslot);
   if (P.mode == MODE_CONF) {
     const int nb = (P.n_cand + 255) / 256;
     e = launch_pdl(lopa_fold_kernel, dim3(nb), dim3(256), 0, s, P);
@@ -1145,6 +1167,44 @@ int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, co
 using namespace lopa;
 
 extern "C" int lopa_version(void) { return LOPA_VERSION; }
+
+extern "C" int lopa_profile_enable(int32_t max_records) {
+  if (max_records < 1) return LOPA_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> lk(lopa::g_prof.mu);
+  if (lopa::g_prof.ev) {
+    for (int i = 0; i < 2 * lopa::g_prof.cap; ++i) cudaEventDestroy(lopa::g_prof.ev[i]);
+    delete[] lopa::g_prof.ev;
+    lopa::g_prof.ev = nullptr;
+  }
+  lopa::g_prof.ev = new cudaEvent_t[2 * max_records];
+  for (int i = 0; i < 2 * max_records; ++i)
+    if (cudaEventCreate(&lopa::g_prof.ev[i]) != cudaSuccess) return LOPA_ERR_CUDA;
+  lopa::g_prof.cap = max_records;
+  lopa::g_prof.n = 0;
+  return LOPA_OK;
+}
+
+extern "C" int lopa_profile_read(float* k1_ms, int32_t max, int32_t* n_out) {
+  if (!k1_ms || !n_out || max < 0) return LOPA_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> lk(lopa::g_prof.mu);
+  *n_out = 0;
+  if (!lopa::g_prof.ev) return LOPA_OK;
+  int st = LOPA_OK;
+  const int n = std::min(max, lopa::g_prof.n);
+  for (int i = 0; i < n; ++i) {
+    if (cudaEventSynchronize(lopa::g_prof.ev[2 * i + 1]) != cudaSuccess ||
+        cudaEventElapsedTime(&k1_ms[i], lopa::g_prof.ev[2 * i], lopa::g_prof.ev[2 * i + 1]) != cudaSuccess) {
+      st = LOPA_ERR_CUDA;
+      break;
+    }
+    *n_out = i + 1;
+  }
+  for (int i = 0; i < 2 * lopa::g_prof.cap; ++i) cudaEventDestroy(lopa::g_prof.ev[i]);
+  delete[] lopa::g_prof.ev;
+  lopa::g_prof.ev = nullptr;
+  lopa::g_prof.cap = lopa::g_prof.n = 0;
+  return st;
+}
 
 // Debug: copy the per-CTA phase timeline of the last launch (timeline builds only; returns the
 // number of slots per CTA, 0 if the build has no timeline).

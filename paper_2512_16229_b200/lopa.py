@@ -76,6 +76,8 @@ _SIGS = {
     "lopa_bp_check": (_i32, [_c_void_p]),
     "lopa_bp_destroy": (None, [_c_void_p]),
     "lopa_debug_timeline": (_i32, [_c_void_p, _i32]),
+    "lopa_profile_enable": (_i32, [_i32]),
+    "lopa_profile_read": (_i32, [ctypes.POINTER(ctypes.c_float), _i32, ctypes.POINTER(_i32)]),
     "lopa_syn_generate": (_i32, [_u64, _i32, _i32, _i64, _i32, _i32, _c_void_p, _c_void_p, _i32,
                                  _c_void_p, _c_void_p]),
 }
@@ -285,6 +287,20 @@ class Stepper:
         a = self.args(logits, n_branches, branch_tokens, branch_mask)
         _check(lib().lopa_step(ctypes.byref(a), _stream(self.device)), "lopa_step")
         return self.out
+
+
+# ----------------------------------------------------------------------------- measurement
+def profile_enable(max_records: int):
+    """Record CUDA events around every K1 (vocabulary reduction) launch of the next calls."""
+    _check(lib().lopa_profile_enable(max_records), "lopa_profile_enable")
+
+
+def profile_read(max_records: int):
+    """Synchronise and return the recorded K1 durations (ms); disables recording."""
+    buf = (ctypes.c_float * max_records)()
+    n = _i32(0)
+    _check(lib().lopa_profile_read(buf, max_records, ctypes.byref(n)), "lopa_profile_read")
+    return list(buf[: n.value])
 
 
 # ----------------------------------------------------------------------------- harness

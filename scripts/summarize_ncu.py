@@ -1,0 +1,65 @@
+"""Summarise ncu outputs from gpurun_out/ into profiles/ (committed evidence).
+
+    python scripts/summarize_ncu.py <round-tag>
+reads gpurun_out/launches.csv (gpu__time_duration per launch) and gpurun_out/prof_full.ncu-rep
+(--set full of the step kernels), writes profiles/<tag>_launches.csv, profiles/<tag>_ncu_summary.md
+and profiles/traffic.json (dram bytes per K1 launch, read by bench.py)."""
+import csv, io, json, os, subprocess, sys
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+go = os.path.join(root, "gpurun_out"); pr = os.path.join(root, "profiles")
+os.makedirs(pr, exist_ok=True)
+out = []
+rows = list(csv.reader(open(os.path.join(go, "launches.csv"))))
+hdr = None; launches = []
+for r in rows:
+    if "Kernel Name" in r: hdr = r; continue
+    if hdr and len(r) == len(hdr):
+        d = dict(zip(hdr, r)); launches.append((d["ID"], d["Kernel Name"], float(d["Metric Value"])))
+with open(os.path.join(pr, f"{tag}_launches.csv"), "w") as f:
+    f.write("id,kernel,gpu__time_duration_ns\n")
+    for i, k, v in launches: f.write(f'{i},"{k}",{v:.0f}\n')
+lk = [v for _, k, v in launches if "lopa_reduce" in k][-20:]
+tk = [v for _, k, v in launches if "lopa_tail" in k][-20:]
+out.append(f"# ncu summary ({tag})\n")
+out.append("Command: `python bench.py --steps 20 --warmup 3 --no-cpu-baseline` (Dream verify step, 241 masked rows x V=151936).\n")
+out.append("## Launch list (gpu__time_duration.sum, --clock-control none; serialised, cold-cache)\n")
+if lk and tk:
+    mk, mt = sum(lk) / len(lk), sum(tk) / len(tk)
+    out.append(f"- K1 lopa_reduce_kernel: mean {mk/1000:.2f} us over the last {len(lk)} launches")
+    out.append(f"- K2 lopa_tail_kernel: mean {mt/1000:.2f} us")
+    out.append(f"- K1 share of the step (K1/(K1+K2)): {mk/(mk+mt):.1%}\n")
+rep = os.path.join(go, "prof_full.ncu-rep")
+traffic = None
+if os.path.exists(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    h = rr[0]
+    want = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+            "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+            "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct"]
+    out.append("## --set full (one launch of each kernel)\n")
+    out.append("| kernel | " + " | ".join(want) + " |")
+    out.append("|---|" + "---|" * len(want))
+    for r in rr[2:]:
+        d = dict(zip(h, r))
+        name = d.get("Kernel Name", "")[:28]
+        vals = [d.get(w, "") for w in want]
+        out.append(f"| {name} | " + " | ".join(vals) + " |")
+        if "lopa_reduce" in name and traffic is None:
+            try:
+                unit_r = rr[1][h.index("dram__bytes_read.sum")]
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
+                traffic = (float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * scale
+            except Exception:
+                traffic = None
+    out.append("")
+    out.append("Units row: " + ", ".join(f"{w}={rr[1][h.index(w)]}" for w in want if w in h))
+if traffic:
+    json.dump({"bytes_per_launch": traffic, "kernel": "lopa_reduce_kernel", "source": f"profiles/{tag}_ncu_summary.md"},
+              open(os.path.join(pr, "traffic.json"), "w"))
+    out.append(f"\nK1 DRAM traffic per launch (read+write): {traffic/1e6:.2f} MB (algorithmic: 73.23 MB)")
+open(os.path.join(pr, f"{tag}_ncu_summary.md"), "w").write("\n".join(out) + "\n")
+print("\n".join(out))
