@@ -99,7 +99,7 @@ struct Params {
   int32_t* argmax;
   int32_t* dev_status;
   uint32_t* ctrs;              // [0] work-item counter, [2] n_masked (K1 -> K2)
-  float4* gpart;               // [n_cand][n_grp] group partials (m, s, argmax bits, -)
+  float4* gpart;               // [n_grp][n_cand] group partials (m, s, argmax bits, -), group-major
   int mode;
   // tails
   const int32_t* branch_tokens;  // global tables [.. ][W]
@@ -275,7 +275,11 @@ __device__ __forceinline__ Partial reduce_slice(const uint8_t* stage, int nchunk
   // exact first argmax: a lane holding the max finds its first chunk containing it and re-reads
   // that chunk from shared memory (the stage is released only afterwards).
   uint32_t cand = 0xFFFFFFFFu;
+#ifdef LOPA_EXP_NOARGMAX
+  if (false) {
+#else
   if (ml == m) {
+#endif
     int tf = kChunksPerLane - 1;
 #pragma unroll
     for (int t = kChunksPerLane - 1; t >= 0; --t)
@@ -696,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
           __threadfence_block();
           const float4* q = ipart + slot * kPartPerItem;
           const FoldAcc f = fold_seq(kWarpsPerSeg * nsi, [&](int p) { return q[p]; });
-          P.gpart[(size_t)row_list[rc] * n_grp + g] = make_float4(f.M, f.S, __uint_as_float(f.a), 0.f);
+          P.gpart[(size_t)g * P.n_cand + row_list[rc]] = make_float4(f.M, f.S, __uint_as_float(f.a), 0.f);
           icnt[slot] = 0;
           mbar_arrive(&slot_free[slot]);
         }
@@ -716,16 +720,18 @@ constexpr int kTailThreads = 512;
 constexpr size_t kTailSmemBytes = kTailBytes + LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW * 2;
 
 
-// Fold one row's group partials (read straight from the workspace, all loads in flight) ->
+// Fold one row's group partials (read straight from the group-major workspace: group g of row r
+// at q[g * stride], so the loads of consecutive rows are coalesced; all loads in flight) ->
 // conf, argmax.  Fixed order: the 16-slot pairwise tree for n_grp <= 16, sequential beyond.
-__device__ __forceinline__ FoldAcc fold_row_global(const float4* q, int n_grp) {
+__device__ __forceinline__ FoldAcc fold_row_global(const float4* q, int n_grp, size_t stride) {
   if (n_grp <= 16) {
     float4 qr[16];
 #pragma unroll
-    for (int p = 0; p < 16; ++p) qr[p] = p < n_grp ? __ldcg(q + p) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = 0; p < 16; ++p)
+      qr[p] = p < n_grp ? __ldcg(q + p * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
     return fold_tree16(n_grp, qr);
   }
-  return fold_seq(n_grp, [&](int p) { return __ldcg(q + p); });
+  return fold_seq(n_grp, [&](int p) { return __ldcg(q + p * stride); });
 }
 
 template <int MODE>
@@ -792,7 +798,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   const int n_grp = P.n_grp;
   for (int rc = tid; rc < n_masked; rc += kTailThreads) {
     const int row = rows[rc];
-    const FoldAcc f = fold_row_global(P.gpart + (size_t)row * n_grp, n_grp);
+    const FoldAcc f = fold_row_global(P.gpart + row, n_grp, (size_t)P.n_cand);
     const float c = __fdiv_rn(1.0f, f.S);
     P.conf[row] = c;
     P.argmax[row] = (int32_t)f.a;
@@ -818,7 +824,7 @@ __global__ void __launch_bounds__(256) lopa_fold_kernel(const Params P) {
   const bool valid = r < P.n_cand && (P.row_mask == nullptr || P.row_mask[r] != 0);
   grid_dep_wait();
   if (valid) {
-    const FoldAcc f = fold_row_global(P.gpart + (size_t)r * P.n_grp, P.n_grp);
+    const FoldAcc f = fold_row_global(P.gpart + r, P.n_grp, (size_t)P.n_cand);
     P.conf[r] = __fdiv_rn(1.0f, f.S);
     P.argmax[r] = (int32_t)f.a;
     if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);

@@ -32,7 +32,7 @@ inline int32_t num_groups(int32_t n_seg) { return (n_seg + kSegPerItem - 1) / kS
 
 struct Workspace {
   uint32_t* ctrs;       // [0] work-item counter (zero between calls)
-  float4* gpart;        // [max_rows][n_groups] group partials, indexed by raw row
+  float4* gpart;        // [n_groups][max_rows] group partials (group-major, raw row index)
 };
 
 size_t workspace_bytes(int32_t max_rows, int32_t vocab);
