@@ -59,7 +59,8 @@ typedef enum {
   LOPA_ERR_INVALID_ARG = 1, /* null pointer, vocab < 1, window < 1, k < 0, tau not in (0,1],
                                ld < vocab, ld % 8 != 0, logits not 16-byte aligned, ...   */
   LOPA_ERR_UNSUPPORTED = 2, /* window > LOPA_MAX_WINDOW, branches > LOPA_MAX_BRANCHES,
-                               rows > LOPA_MAX_ROWS, device is not sm_100                  */
+                               rows > LOPA_MAX_ROWS, vocab > LOPA_MAX_VOCAB, device is not
+                               sm_100                                                      */
   LOPA_ERR_CUDA = 3,        /* a CUDA runtime error (launch / capture)                     */
   LOPA_ERR_NCCL = 4         /* an NCCL error in the branch-parallel exchange               */
 } lopa_status_t;
@@ -72,6 +73,7 @@ typedef enum {
 #define LOPA_MAX_WINDOW 64    /* W <= 64: one warp owns a window (NEXT-1 lifts this)        */
 #define LOPA_MAX_BRANCHES 32  /* k + 1 <= 32: one lane per branch in the select             */
 #define LOPA_MAX_ROWS 4096    /* rows per lopa_confidence call                              */
+#define LOPA_MAX_VOCAB (1 << 23) /* conf >= 1/V >= 2^-23 keeps the fp64 Eq. 2 sums exact       */
 
 int lopa_version(void);
 const char* lopa_status_string(int status);

@@ -1093,7 +1093,7 @@ int validate_step_args(const lopa_step_args_t* a, bool need_next) {
   if (need_next && (!a->scores || !a->winner || !a->next_tokens || !a->next_mask ||
                     !a->n_branches_next || (a->k > 0 && !a->lookahead_pos)))
     return LOPA_ERR_INVALID_ARG;
-  if (a->window > LOPA_MAX_WINDOW) return LOPA_ERR_UNSUPPORTED;
+  if (a->window > LOPA_MAX_WINDOW || a->vocab > LOPA_MAX_VOCAB) return LOPA_ERR_UNSUPPORTED;
   if (a->max_branches > LOPA_MAX_BRANCHES || a->k + 1 > LOPA_MAX_BRANCHES)
     return LOPA_ERR_UNSUPPORTED;
   return LOPA_OK;
@@ -1256,7 +1256,7 @@ extern "C" int lopa_confidence(const void* logits, int64_t ld, int32_t n_rows, i
   if (n_rows < 0) return LOPA_ERR_INVALID_ARG;
   if (!logits_ok(logits, ld, vocab) || !conf || !argmax || !dev_status || !workspace)
     return LOPA_ERR_INVALID_ARG;
-  if (n_rows > LOPA_MAX_ROWS) return LOPA_ERR_UNSUPPORTED;
+  if (n_rows > LOPA_MAX_ROWS || vocab > LOPA_MAX_VOCAB) return LOPA_ERR_UNSUPPORTED;
   if (n_rows == 0) return LOPA_OK;
   Workspace ws;
   if (!carve_workspace(workspace, workspace_bytes, n_rows, vocab, &ws)) return LOPA_ERR_INVALID_ARG;
