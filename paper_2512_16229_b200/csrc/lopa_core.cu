@@ -274,41 +274,53 @@ __device__ __forceinline__ Partial reduce_slice(const uint8_t* stage, int nchunk
   }
   // exact first argmax: a lane holding the max finds its first chunk containing it and re-reads
   // that chunk from shared memory (the stage is released only afterwards).
-  uint32_t cand = 0xFFFFFFFFu;
-#ifdef LOPA_EXP_NOARGMAX
-  if (false) {
-#else
-  if (ml == m) {
+  auto argmax_cand = [&]() -> uint32_t {
+    uint32_t cand = 0xFFFFFFFFu;
+#ifndef LOPA_EXP_NOARGMAX
+    if (ml == m) {
+      int tf = kChunksPerLane - 1;
+#pragma unroll
+      for (int t = kChunksPerLane - 1; t >= 0; --t)
+        if (fmaxf(bf16lo(cm[t]), bf16hi(cm[t])) == m) tf = t;
+      const int c = 128 * tf + 32 * wq + lane;
+      uint4 w = lds128(buf + c);
+      if (ragged) {
+        const int nvalid = vocab - (e0 + 8 * c);
+        if (nvalid < 8) mask_tail(w, nvalid);
+      }
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      int ef = 7;
+#pragma unroll
+      for (int e = 7; e >= 0; --e) {
+        const float x = (e & 1) ? bf16hi(ws[e >> 1]) : bf16lo(ws[e >> 1]);
+        if (x == m) ef = e;
+      }
+      cand = (uint32_t)(e0 + 8 * c + ef);
+    }
 #endif
-    int tf = kChunksPerLane - 1;
-#pragma unroll
-    for (int t = kChunksPerLane - 1; t >= 0; --t)
-      if (fmaxf(bf16lo(cm[t]), bf16hi(cm[t])) == m) tf = t;
-    const int c = 128 * tf + 32 * wq + lane;
-    uint4 w = lds128(buf + c);
-    if (ragged) {
-      const int nvalid = vocab - (e0 + 8 * c);
-      if (nvalid < 8) mask_tail(w, nvalid);
-    }
-    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-    int ef = 7;
-#pragma unroll
-    for (int e = 7; e >= 0; --e) {
-      const float x = (e & 1) ? bf16hi(ws[e >> 1]) : bf16lo(ws[e >> 1]);
-      if (x == m) ef = e;
-    }
-    cand = (uint32_t)(e0 + 8 * c + ef);
-  }
-  __syncwarp();
-  if (lane == 0) mbar_arrive(empty_bar);
-  p.a = __reduce_min_sync(0xffffffffu, cand);
+    return cand;
+  };
   // sum of exp(x - m) in a fixed order: packed tree inside a chunk, chunks in t order, then
   // (.x + .y), then a butterfly over lanes (identical bits in every lane)
-  const float negm = -m;
-  float2 acc = chunk_exp_sum2(v[0], negm);
+  auto exp_sum = [&]() -> float {
+    const float negm = -m;
+    float2 acc = chunk_exp_sum2(v[0], negm);
 #pragma unroll
-  for (int t = 1; t < kChunksPerLane; ++t) acc = __fadd2_rn(acc, chunk_exp_sum2(v[t], negm));
-  float ls = acc.x + acc.y;
+    for (int t = 1; t < kChunksPerLane; ++t) acc = __fadd2_rn(acc, chunk_exp_sum2(v[t], negm));
+    return acc.x + acc.y;
+  };
+#ifdef LOPA_LATE_ARGMAX
+  float ls = exp_sum();
+  const uint32_t cand = argmax_cand();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_bar);
+#else
+  const uint32_t cand = argmax_cand();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_bar);
+  float ls = exp_sum();
+#endif
+  p.a = __reduce_min_sync(0xffffffffu, cand);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
   p.s = ls;
