@@ -402,3 +402,65 @@ def test_invalid_args_raise(L):
                                                 torch.ones((2, 65), dtype=torch.uint8, device=DEV))
     with pytest.raises(L.LopaError):
         L.confidence(torch.zeros((2, 64)))  # CPU tensor: no fallback
+
+
+# ----------------------------------------------------------------------------- multi-block loops
+def _gpu_decode_blocks(L, seed, V, W, k, tau, n_blocks, extras=0):
+    toks, fw = [], 0
+    for blk in range(n_blocks):
+        t, f = _gpu_decode_block(L, seed, V, W, k, tau, extras, blk=blk)
+        toks.append(t)
+        fw += f
+    return np.concatenate(toks), fw
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_multiblock_decode_toy(L, seed):
+    """Sequential blocks (R18/R22: each block starts from its own initial forward)."""
+    V, W, k, tau = 64, 8, 2, 0.9
+    ref_tok, ref_fw = [], 0
+    for blk in range(4):
+        fwd = lambda t, m, blk=blk: syngen.gen_logits(seed, blk, V, t, m, extras=1)
+        tok0, msk0 = syngen.fresh_block(W)
+        tr = O.decode_block(fwd, tok0, msk0, k, tau)
+        ref_tok.append(tr.tokens)
+        ref_fw += tr.forwards
+    g_tok, g_fw = _gpu_decode_blocks(L, seed, V, W, k, tau, 4, extras=1)
+    assert g_fw == ref_fw and np.array_equal(g_tok, np.concatenate(ref_tok))
+
+
+def test_multiblock_decode_diffucoder(L):
+    """D2F-DiffuCoder shape (configs[3]): V=151936, W=32, k=10, tau=0.95, 2 sequential blocks
+    (64 tokens), final tokens and forward counts equal to the oracle's."""
+    V, W, k, tau, seed = 151936, 32, 10, 0.95, 3
+    ref_tok, ref_fw = [], 0
+    for blk in range(2):
+        fwd = lambda t, m, blk=blk: syngen.gen_logits(seed, blk, V, t, m)
+        tok0, msk0 = syngen.fresh_block(W)
+        tr = O.decode_block(fwd, tok0, msk0, k, tau)
+        ref_tok.append(tr.tokens)
+        ref_fw += tr.forwards
+    g_tok, g_fw = _gpu_decode_blocks(L, seed, V, W, k, tau, 2)
+    assert g_fw == ref_fw and np.array_equal(g_tok, np.concatenate(ref_tok))
+
+
+@pytest.mark.parametrize("k,W", [(1, 16), (3, 16), (15, 32), (31, 64), (31, 16)])
+def test_sweep_shapes_one_step(L, k, W):
+    """BASELINE configs[4] sweep shapes (k in {1,3,15,31} x W in {16,32,64}) at V=151936: one
+    verify step after the initial anchor, compared with the oracle."""
+    _run_steps(L, 7, 151936, W, k, 0.9, 2, extras=0)
+
+
+def test_dense_rows_roofline_mode(L):
+    """Dense mode of the bench roofline (every (branch, position) row masked): a1 over 256 rows
+    equals the oracle on sampled rows."""
+    V, W, k = 151936, 32, 7
+    tok = torch.zeros((k + 1, W), dtype=torch.int32, device=DEV)
+    msk = torch.ones((k + 1, W), dtype=torch.uint8, device=DEV)
+    x = L.syn_generate(21, 0, V, tok, msk).view((k + 1) * W, -1)
+    c, a, st = L.confidence(x)
+    assert int(st.item()) == 0
+    xs = G.to_np_u16(x)
+    for r in (0, 77, 128, 255):
+        rc, ra, _ = O.row_confidence(xs[r])
+        assert abs(c[r].item() - rc) <= 2e-6 and a[r].item() == ra
