@@ -26,6 +26,8 @@
 #include <cstring>
 #include <mutex>
 
+#include <cuda_bf16.h>
+
 #include "liblopa.h"
 #include "lopa_ptx.cuh"
 namespace lopa {
@@ -189,13 +191,41 @@ __device__ __forceinline__ float2 ex2x2(float2 d) {
   return make_float2(ex2(z.x), ex2(z.y));
 }
 
+// 2^x on the FMA pipe (the "FA4 trick": relieves the MUFU/XU pipe): x = j + f, j = rint(x),
+// f in [-0.5, 0.5]; 2^f by a degree-5 fit (max rel. error 3e-7 in fp32, like ex2.approx);
+// 2^j added to the exponent field.  x is clamped at -126 (the term is then < 2^-125, far below
+// one ulp of the sum S >= 1).  NaN inputs need no care: a NaN in a slice makes its max NaN
+// (max.NaN.bf16x2), which poisons the whole slice through the MUFU path.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  const float2 xc = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 r = __fadd2_rn(xc, magic);
+  const float2 jf = __fadd2_rn(r, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(xc, make_float2(-jf.x, -jf.y));
+  float2 p = make_float2(0.0013260914711281657f, 0.0013260914711281657f);
+  p = __ffma2_rn(p, f, make_float2(0.009670180268585682f, 0.009670180268585682f));
+  p = __ffma2_rn(p, f, make_float2(0.055507123470306396f, 0.055507123470306396f));
+  p = __ffma2_rn(p, f, make_float2(0.2402222454547882f, 0.2402222454547882f));
+  p = __ffma2_rn(p, f, make_float2(0.6931470036506653f, 0.6931470036506653f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  const int jx = __float_as_int(r.x) - 0x4B400000, jy = __float_as_int(r.y) - 0x4B400000;
+  return make_float2(__int_as_float(__float_as_int(p.x) + (jx << 23)),
+                     __int_as_float(__float_as_int(p.y) + (jy << 23)));
+}
+
+#ifndef LOPA_POLY_WORDS
+#define LOPA_POLY_WORDS 0  // words (of 4 per chunk) whose two exps use ex2_poly2
+#endif
+
 // Sum of exp(x - m) over one 16-byte chunk (8 elements), in the fixed packed order
-// ((e0,e1) + (e2,e3)) + ((e4,e5) + (e6,e7)) as float2 pairs.
+// ((e0,e1) + (e2,e3)) + ((e4,e5) + (e6,e7)) as float2 pairs.  Which words take the polynomial
+// is fixed by position, so the result is still a function of the chunk's bytes only.
 __device__ __forceinline__ float2 chunk_exp_sum2(const uint4& v, float negm) {
+  const float2 L2 = make_float2(kLog2e, kLog2e);
   const float2 p0 = ex2x2(minus_m(v.x, negm));
-  const float2 p1 = ex2x2(minus_m(v.y, negm));
-  const float2 p2 = ex2x2(minus_m(v.z, negm));
-  const float2 p3 = ex2x2(minus_m(v.w, negm));
+  const float2 p1 = LOPA_POLY_WORDS >= 3 ? ex2_poly2(__fmul2_rn(minus_m(v.y, negm), L2)) : ex2x2(minus_m(v.y, negm));
+  const float2 p2 = LOPA_POLY_WORDS >= 2 ? ex2_poly2(__fmul2_rn(minus_m(v.z, negm), L2)) : ex2x2(minus_m(v.z, negm));
+  const float2 p3 = LOPA_POLY_WORDS >= 1 ? ex2_poly2(__fmul2_rn(minus_m(v.w, negm), L2)) : ex2x2(minus_m(v.w, negm));
   return __fadd2_rn(__fadd2_rn(p0, p1), __fadd2_rn(p2, p3));
 }
 
@@ -257,7 +287,7 @@ __device__ __forceinline__ Partial reduce_slice(const uint8_t* stage, int nchunk
   uint32_t mm = cm[0];
 #pragma unroll
   for (int t = 1; t < kChunksPerLane; ++t) mm = bmax2(mm, cm[t]);
-  const float ml = fmaxf(bf16lo(mm), bf16hi(mm));
+  const float ml = fmax_nan(bf16lo(mm), bf16hi(mm));  // NaN-propagating, like bmax2
   const float m = unordered(__reduce_max_sync(0xffffffffu, ordered_bits(ml)));
 
   Partial p;
@@ -278,10 +308,12 @@ __device__ __forceinline__ Partial reduce_slice(const uint8_t* stage, int nchunk
     uint32_t cand = 0xFFFFFFFFu;
 #ifndef LOPA_EXP_NOARGMAX
     if (ml == m) {
+      // packed bf16x2 compares against (m, m): m is a bf16 value, and -0 == +0 as in IEEE
+      const __nv_bfloat162 m2 = __floats2bfloat162_rn(m, m);
       int tf = kChunksPerLane - 1;
 #pragma unroll
       for (int t = kChunksPerLane - 1; t >= 0; --t)
-        if (fmaxf(bf16lo(cm[t]), bf16hi(cm[t])) == m) tf = t;
+        if (!__hbne2(*reinterpret_cast<const __nv_bfloat162*>(&cm[t]), m2)) tf = t;
       const int c = 128 * tf + 32 * wq + lane;
       uint4 w = lds128(buf + c);
       if (ragged) {
@@ -291,9 +323,9 @@ __device__ __forceinline__ Partial reduce_slice(const uint8_t* stage, int nchunk
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
       int ef = 7;
 #pragma unroll
-      for (int e = 7; e >= 0; --e) {
-        const float x = (e & 1) ? bf16hi(ws[e >> 1]) : bf16lo(ws[e >> 1]);
-        if (x == m) ef = e;
+      for (int j = 3; j >= 0; --j) {
+        const unsigned eq = __heq2_mask(*reinterpret_cast<const __nv_bfloat162*>(&ws[j]), m2);
+        if (eq) ef = 2 * j + ((eq & 0xFFFFu) ? 0 : 1);
       }
       cand = (uint32_t)(e0 + 8 * c + ef);
     }

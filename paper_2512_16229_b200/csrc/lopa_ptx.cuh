@@ -75,10 +75,16 @@ __device__ __forceinline__ int32_t ldcg_i32(const int32_t* p) { return __ldcg(p)
 __device__ __forceinline__ float4 ldcg_f4(const float4* p) { return __ldcg(p); }
 
 // ---- bf16x2 --------------------------------------------------------------------------------
-// max.bf16x2 (NaN-dropping): exact; NaNs are detected later through the exp-sum.
+// max.NaN.bf16x2: exact, and a NaN anywhere makes the result NaN (the slice's max, and through
+// it the whole slice's exp-sum, become NaN: the row is reported non-finite).
 __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
   uint32_t d;
-  asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
   return d;
 }
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
