@@ -165,12 +165,37 @@ def spawn_branches(conf, argmax, tokens_b0, mask_b0, k: int) -> Spawn:
 
 
 # ----------------------------------------------------------------------------- Eq. 2 + select
-def branch_score(conf_row, mask_row) -> float:
-    """Eq. 2: mean of Conf over the branch's own unfilled positions; 1.0 if none (R8)."""
+METRIC_MEAN = 0            # Eq. 2
+METRIC_SLIDING_MIN = 1     # P:204 "applying a sliding window to assess local quality"
+METRIC_BOTTOM_FRACTION = 2 # P:204 "averaging confidence over the least confident segment"
+
+
+def branch_score(conf_row, mask_row, metric: int = METRIC_MEAN, param: float = 0.0) -> float:
+    """Branch confidence C(B_j) over the branch's own unfilled positions M_Bj, in position order.
+
+    * METRIC_MEAN: Eq. 2, the arithmetic mean.
+    * METRIC_SLIDING_MIN: the minimum over all length-w contiguous windows of
+      the window mean, w = param clamped to |M_Bj| (reading R23: windows over the unfilled
+      positions in position order, as S:228 states).
+    * METRIC_BOTTOM_FRACTION: the mean of the ceil(eta * |M_Bj|) lowest
+      confidences, eta = param (fp32, R14-style: ceil of (double)(float)eta * n, exact).
+    1.0 if M_Bj is empty (R8).
+    """
     vals = [float(conf_row[i]) for i in range(len(mask_row)) if mask_row[i]]
     if not vals:
         return 1.0
-    return float(sum(vals) / len(vals))
+    n = len(vals)
+    if metric == METRIC_MEAN:
+        return float(sum(vals) / n)
+    if metric == METRIC_SLIDING_MIN:
+        w = min(int(param), n)
+        return float(min(sum(vals[s:s + w]) / w for s in range(n - w + 1)))
+    if metric == METRIC_BOTTOM_FRACTION:
+        import math
+        b = int(math.ceil(float(np.float32(param)) * n))
+        low = sorted(vals)[:b]
+        return float(sum(low) / b)
+    raise ValueError("unknown branch-confidence metric")
 
 
 def verify_select(scores) -> int:
@@ -196,7 +221,8 @@ class StepResult:
         return 0 if self.done else len(self.spawn.lookahead) + 1
 
 
-def step(logits_u16, branch_tokens, branch_mask, k: int, tau) -> StepResult:
+def step(logits_u16, branch_tokens, branch_mask, k: int, tau, metric: int = METRIC_MEAN,
+         param: float = 0.0) -> StepResult:
     """One LoPA verify step over n_br branches' verify logits [n_br][W][>=V] (§8(a) a1-a4).
 
     a1 Conf/argmax of every masked (branch, position) row ("Compute scores ... Single
@@ -212,7 +238,7 @@ def step(logits_u16, branch_tokens, branch_mask, k: int, tau) -> StepResult:
         c, a, st = confidence(L[j], branch_mask[j])
         conf[j], amax[j] = c, a
         status |= st
-    scores = [branch_score(conf[j], branch_mask[j]) for j in range(n_br)]
+    scores = [branch_score(conf[j], branch_mask[j], metric, param) for j in range(n_br)]
     w = verify_select(scores)
     if not np.asarray(branch_mask[w]).any():
         return StepResult(conf, amax, scores, w, True, None, None, status)

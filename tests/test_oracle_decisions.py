@@ -162,3 +162,45 @@ def test_scores_match_exact_rationals():
         w = O.verify_select(ours)
         assert w == brute.brute_winner(exact)
         assert all(ours[w] >= s for s in ours)
+
+
+# ----------------------------------------------------------------------------- Eq. 2 variants
+def test_spec_sliding_window_example():
+    """confs in position order [.9,.2,.8], sliding_window(2) -> min(.55, .5) = 0.5."""
+    conf = np.array([0.9, 0.2, 0.8])
+    mask = np.ones(3, dtype=np.uint8)
+    assert O.branch_score(conf, mask, O.METRIC_SLIDING_MIN, 2) == pytest.approx(0.5, abs=1e-15)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_metric_variants_reduce_and_bound(seed):
+    """Closed-form reductions of the Eq. 2 variants, exact rational checks, and
+    the ordering min <= bottom-fraction <= mean <= ... that any correct implementation obeys."""
+    rng = random.Random(seed)
+    W = rng.randint(1, 20)
+    conf = np.array([float(np.float32(rng.random())) for _ in range(W)])
+    mask = np.array([rng.random() < 0.7 for _ in range(W)], dtype=np.uint8)
+    vals = [conf[i] for i in range(W) if mask[i]]
+    if not vals:
+        for m, p in ((O.METRIC_SLIDING_MIN, 3), (O.METRIC_BOTTOM_FRACTION, 0.5)):
+            assert O.branch_score(conf, mask, m, p) == 1.0
+        return
+    n = len(vals)
+    mean = O.branch_score(conf, mask)
+    # window >= n -> the mean; window 1 -> the minimum
+    assert O.branch_score(conf, mask, O.METRIC_SLIDING_MIN, n + 3) == mean
+    assert O.branch_score(conf, mask, O.METRIC_SLIDING_MIN, 1) == min(vals)
+    # eta = 1 -> the mean; eta -> 0+ -> the minimum
+    assert O.branch_score(conf, mask, O.METRIC_BOTTOM_FRACTION, 1.0) == pytest.approx(mean, abs=1e-15)
+    assert O.branch_score(conf, mask, O.METRIC_BOTTOM_FRACTION, 1e-6) == min(vals)
+    # exact rational recompute of a window / bottom mean
+    w = rng.randint(1, n)
+    exact_w = min(sum(Fraction(v) for v in vals[s:s + w]) / w for s in range(n - w + 1))
+    assert abs(O.branch_score(conf, mask, O.METRIC_SLIDING_MIN, w) - float(exact_w)) < 1e-15
+    eta = float(np.float32(rng.random()))
+    b = -(-(Fraction(eta) * n).numerator // (Fraction(eta) * n).denominator)   # exact ceil
+    exact_b = sum(sorted(Fraction(v) for v in vals)[:b]) / b
+    assert abs(O.branch_score(conf, mask, O.METRIC_BOTTOM_FRACTION, eta) - float(exact_b)) < 1e-15
+    # ordering
+    assert min(vals) <= O.branch_score(conf, mask, O.METRIC_SLIDING_MIN, w) <= max(vals)
+    assert min(vals) <= O.branch_score(conf, mask, O.METRIC_BOTTOM_FRACTION, eta) <= mean + 1e-15
