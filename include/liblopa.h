@@ -131,7 +131,21 @@ int lopa_verify_select(const float* conf, const uint8_t* branch_mask, const int3
                        int32_t max_branches, int32_t window, float* scores, int32_t* winner,
                        void* stream);
 
-/* One fused verify step (a1 -> a2 -> a3 -> a4) in a single kernel launch. */
+/* Branch-confidence metrics.  The Eq. 2 mean is the paper's default; the
+ * two variants are the ones P:204 names.  All are computed from exact fp64 sums. */
+#define LOPA_METRIC_MEAN 0            /* C(B_j) = mean of Conf over M_Bj (Eq. 2)                 */
+#define LOPA_METRIC_SLIDING_MIN 1     /* min over length-w windows of M_Bj (position order) of the
+                                         window mean; w clamped to |M_Bj| ("local quality")     */
+#define LOPA_METRIC_BOTTOM_FRACTION 2 /* mean of the ceil(eta |M_Bj|) lowest confidences
+                                         ("least confident segment")                            */
+
+/* a2 with a metric: as lopa_verify_select, scores by `metric` / `metric_param`. */
+int lopa_verify_select_ex(const float* conf, const uint8_t* branch_mask, const int32_t* n_branches,
+                          int32_t max_branches, int32_t window, int32_t metric, float metric_param,
+                          float* scores, int32_t* winner, void* stream);
+
+/* One verify step (a1 -> a2 -> a3 -> a4): the streaming reduction kernel and the fold/decision
+ * kernel, launched back to back (programmatic dependent launch) on `stream`. */
 typedef struct {
   /* inputs */
   const void* logits;            /* device bf16 [max_branches][window][ld]: verify logits     */
@@ -157,6 +171,8 @@ typedef struct {
   int32_t* dev_status;           /* scalar, LOPA_DEV_* bits                                  */
   void* workspace;
   size_t workspace_bytes;        /* >= lopa_workspace_bytes(max_branches * window, vocab)   */
+  int32_t metric;                /* branch confidence: LOPA_METRIC_* (0 = Eq. 2 mean)        */
+  float metric_param;            /* window w >= 1 (integer) or eta in (0, 1]; unused for mean */
 } lopa_step_args_t;
 
 /* Next tables must not alias the input tables.  Errors: INVALID_ARG, UNSUPPORTED, CUDA. */

@@ -108,6 +108,8 @@ struct Params {
   const uint8_t* branch_mask;
   int32_t k;
   float tau;
+  int32_t metric;              // branch-confidence metric (kMetric*)
+  float metric_param;          // window w (sliding) or eta (bottom fraction)
   float* scores;
   int32_t* winner;
   int32_t* next_tokens;
@@ -419,34 +421,23 @@ struct TailSmem {
   int32_t rank[LOPA_MAX_WINDOW];
   int32_t n;       // lookahead count, -1 = winner complete
   int32_t best;    // (BP) local best
+  double dscr[16][LOPA_MAX_WINDOW];  // per-warp metric scratch (warps 0..15)
+  float fscr[16][LOPA_MAX_WINDOW];
 };
 constexpr size_t kTailBytes = (sizeof(TailSmem) + 127) / 128 * 128;
 
-// Eq. 2 for branches [0, cap) of the staged table (nb present): warp w scores w, w + kWarps, ...
-// The fp64 sum of <= 64 confidences, each >= 1/V >= 2^-23, is exact in any order.
+// Eq. 2 (or a variant) for branches [0, cap) of the staged table (nb present): warp w
+// scores branches w, w + NT/32, ... (warp_metric_score: exact fp64 sums).
 template <int NT>
-__device__ __forceinline__ void cta_scores(TailSmem& T, int cap, int nb, int W, int warp,
+__device__ __forceinline__ void cta_scores(TailSmem& T, const Params& P, int nb, int W, int warp,
                                            int lane, float* out) {
-  for (int j = warp; j < cap; j += NT / 32) {
-    double s = 0.0;
-    int c = 0;
-    if (j < nb) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = lane + 32 * h;
-        if (i < W) {
-          s += (double)T.conf[j * W + i];
-          c += T.msk[j * W + i];
-        }
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      s += __shfl_xor_sync(0xffffffffu, s, off);
-      c += __shfl_xor_sync(0xffffffffu, c, off);
-    }
+  static_assert(NT / 32 <= 16, "metric scratch holds 16 warps");
+  for (int j = warp; j < P.cap; j += NT / 32) {
+    float sc = -INFINITY;
+    if (j < nb)
+      sc = warp_metric_score(T.conf + j * W, T.msk + j * W, W, P.metric, P.metric_param,
+                             T.dscr[warp], T.fscr[warp], lane);
     if (lane == 0) {
-      const float sc = j < nb ? (c ? (float)(s / (double)c) : 1.0f) : -INFINITY;
       T.scores[j] = sc;
       if (out) out[j] = sc;
     }
@@ -459,7 +450,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
   const int warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
   const int nb = max(0, min(*P.n_branches, P.cap));
-  cta_scores<NT>(T, P.cap, nb, W, warp, lane, P.scores);
+  cta_scores<NT>(T, P, nb, W, warp, lane, P.scores);
   __syncthreads();
   TL(7);
   if (warp == 0) {
@@ -544,7 +535,7 @@ __device__ void cta_tail_bp_local(const Params& P, TailSmem& T, int tid) {
   const int W = P.window;
   const int nb = max(0, min(*P.n_branches - P.branch_base, P.cap));
   RecordView rv = record_view(P.record, P.cap);
-  cta_scores<NT>(T, P.cap, nb, W, warp, lane, rv.scores);
+  cta_scores<NT>(T, P, nb, W, warp, lane, rv.scores);
   __syncthreads();
   if (warp == 0) {
     const float sc = lane < P.cap ? T.scores[lane] : -INFINITY;
@@ -915,6 +906,27 @@ __global__ void verify_kernel(const float* conf, const uint8_t* mask, const int3
   if (lane == 0) *winner = w;
 }
 
+// Eq. 2 variants for the standalone call: one warp scores every branch in turn.
+__global__ void verify_ex_kernel(const float* conf, const uint8_t* mask, const int32_t* n_branches,
+                                 int max_br, int W, int metric, float param, float* scores,
+                                 int32_t* winner) {
+  __shared__ double dscr[LOPA_MAX_WINDOW];
+  __shared__ float fscr[LOPA_MAX_WINDOW];
+  const int lane = threadIdx.x;
+  const int nb = max(0, min(*n_branches, max_br));
+  float mine = -INFINITY;
+  for (int j = 0; j < max_br; ++j) {
+    float sc = -INFINITY;
+    if (j < nb)
+      sc = warp_metric_score(conf + (size_t)j * W, mask + (size_t)j * W, W, metric, param, dscr,
+                             fscr, lane);
+    if (lane == 0) scores[j] = sc;
+    if (lane == j) mine = sc;
+  }
+  const int w = warp_select(mine, lane, nb);
+  if (lane == 0) *winner = w;
+}
+
 // Global half of a BP step: one warp; lane r reads record r's header.
 __global__ void bp_finish_kernel(const Params P, const uint8_t* records, int world, int b_loc,
                                  int n_scores) {
@@ -1121,6 +1133,13 @@ static int launch_reduce(const Params& P, int device, cudaStream_t s) {
   return cuda_status(e);
 }
 
+static bool metric_ok(int32_t metric, float param) {
+  if (metric == LOPA_METRIC_MEAN) return true;
+  if (metric == LOPA_METRIC_SLIDING_MIN) return param >= 1.f && param <= 1e6f && param == (float)(int)param;
+  if (metric == LOPA_METRIC_BOTTOM_FRACTION) return param > 0.f && param <= 1.f;
+  return false;
+}
+
 static bool logits_ok(const void* logits, int64_t ld, int32_t vocab) {
   return logits && vocab >= 1 && ld >= vocab && (ld % 8) == 0 &&
          (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
@@ -1131,6 +1150,7 @@ int validate_step_args(const lopa_step_args_t* a, bool need_next) {
   if (!logits_ok(a->logits, a->ld, a->vocab)) return LOPA_ERR_INVALID_ARG;
   if (a->window < 1 || a->max_branches < 1 || a->k < 0) return LOPA_ERR_INVALID_ARG;
   if (!(a->tau > 0.f && a->tau <= 1.f)) return LOPA_ERR_INVALID_ARG;
+  if (!metric_ok(a->metric, a->metric_param)) return LOPA_ERR_INVALID_ARG;
   if (!a->n_branches || !a->branch_tokens || !a->branch_mask || !a->conf || !a->argmax ||
       !a->dev_status || !a->workspace)
     return LOPA_ERR_INVALID_ARG;
@@ -1162,6 +1182,8 @@ static Params base_params(const lopa_step_args_t* a, const Workspace& ws) {
   P.branch_mask = a->branch_mask;
   P.k = a->k;
   P.tau = a->tau;
+  P.metric = a->metric;
+  P.metric_param = a->metric_param;
   P.scores = a->scores;
   P.winner = a->winner;
   P.next_tokens = a->next_tokens;
@@ -1371,6 +1393,21 @@ extern "C" int lopa_verify_select(const float* conf, const uint8_t* branch_mask,
   verify_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(conf, branch_mask, n_branches,
                                                                   max_branches, window, scores,
                                                                   winner);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int lopa_verify_select_ex(const float* conf, const uint8_t* branch_mask,
+                                     const int32_t* n_branches, int32_t max_branches,
+                                     int32_t window, int32_t metric, float metric_param,
+                                     float* scores, int32_t* winner, void* stream) {
+  if (!conf || !branch_mask || !n_branches || !scores || !winner) return LOPA_ERR_INVALID_ARG;
+  if (window < 1 || max_branches < 1 || !metric_ok(metric, metric_param))
+    return LOPA_ERR_INVALID_ARG;
+  if (window > LOPA_MAX_WINDOW || max_branches > LOPA_MAX_BRANCHES) return LOPA_ERR_UNSUPPORTED;
+  int dev;
+  if (!bind_device(stream, conf, &dev)) return LOPA_ERR_CUDA;
+  verify_ex_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      conf, branch_mask, n_branches, max_branches, window, metric, metric_param, scores, winner);
   return cuda_status(cudaGetLastError());
 }
 

@@ -69,6 +69,92 @@ __device__ __forceinline__ float warp_branch_score(const float* conf, const uint
   return score;
 }
 
+// Branch-confidence metrics.
+constexpr int kMetricMean = 0;            // Eq. 2: mean over M_Bj
+constexpr int kMetricSlidingMin = 1;      // min over length-w windows (position order) of the mean
+constexpr int kMetricBottomFraction = 2;  // mean of the ceil(eta * |M_Bj|) lowest confidences
+
+// C(B_j) of one branch with a full warp (lane owns positions lane and lane + 32).  conf / mask are
+// generic pointers; dscr (64 doubles) and fscr (64 floats) are per-warp shared scratch.  Every sum
+// is an exact fp64 sum (each conf lies in [2^-23, 1], at most 64 terms), so the value equals the
+// oracle's fp64 value whatever the summation order, rounded once to fp32.  1.0 if M_Bj is empty.
+__device__ __forceinline__ float warp_metric_score(const float* conf, const uint8_t* mask, int W,
+                                                   int metric, float param, double* dscr,
+                                                   float* fscr, int lane) {
+  bool m[2];
+  double v[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = lane + 32 * h;
+    m[h] = i < W && mask[i] != 0;
+    v[h] = m[h] ? (double)conf[i] : 0.0;
+  }
+  const uint32_t b0 = __ballot_sync(0xffffffffu, m[0]), b1 = __ballot_sync(0xffffffffu, m[1]);
+  const int n = __popc(b0) + __popc(b1);
+  if (n == 0) return 1.0f;
+  if (metric == kMetricMean) {
+    double s = v[0] + v[1];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    return (float)(s / (double)n);
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+  const int idx[2] = {__popc(b0 & lt), __popc(b0) + __popc(b1 & lt)};
+  float result;
+  if (metric == kMetricSlidingMin) {
+    const int w = min(max((int)param, 1), n);
+    // inclusive prefix sums in position (= compacted) order, stored by compacted index
+    double P[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double x = v[h];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      P[h] = x;
+    }
+    P[1] += __shfl_sync(0xffffffffu, P[0], 31);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (m[h]) dscr[idx[h]] = P[h];
+    __syncwarp();
+    double best = INFINITY;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (m[h] && idx[h] >= w - 1) {
+        const double lo = idx[h] - w >= 0 ? dscr[idx[h] - w] : 0.0;
+        best = fmin(best, (P[h] - lo) / (double)w);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, off));
+    result = (float)best;
+  } else {  // kMetricBottomFraction
+    const int b = (int)ceil((double)param * (double)n);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (m[h]) fscr[idx[h]] = (float)v[h];
+    __syncwarp();
+    double s = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (m[h]) {
+        const float x = (float)v[h];
+        int r = 0;
+        for (int q = 0; q < n; ++q) r += (fscr[q] < x || (fscr[q] == x && q < idx[h])) ? 1 : 0;
+        if (r < b) s += v[h];
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    result = (float)(s / (double)b);
+  }
+  __syncwarp();
+  return result;
+}
+
 // Select (R9): smallest j with the largest fp32 score.  Scores are never NaN-free
 // guaranteed (a NONFINITE row poisons its branch); NaN scores lose (treated as -inf).
 __device__ __forceinline__ int warp_select(float score, int lane, int n_lanes_valid) {

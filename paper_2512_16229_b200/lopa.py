@@ -21,6 +21,9 @@ if os.environ.get("LOPA_LIB_VARIANT"):   # tuning builds (paper_2512_16229_b200/
     LIB_PATH = os.path.join(_PKG, f"liblopa_{os.environ['LOPA_LIB_VARIANT']}.so")
 
 LOPA_OK = 0
+METRIC_MEAN = 0            # Eq. 2
+METRIC_SLIDING_MIN = 1     # P:204 sliding window
+METRIC_BOTTOM_FRACTION = 2 # P:204 least-confident segment
 DEV_EMPTY_MASK = 1
 DEV_NONFINITE = 2
 MAX_WINDOW = 64
@@ -50,6 +53,7 @@ class StepArgs(ctypes.Structure):
         ("next_tokens", _c_void_p), ("next_mask", _c_void_p), ("lookahead_pos", _c_void_p),
         ("n_branches_next", _c_void_p), ("dev_status", _c_void_p),
         ("workspace", _c_void_p), ("workspace_bytes", _size),
+        ("metric", _i32), ("metric_param", _f32),
     ]
 
 
@@ -66,6 +70,8 @@ _SIGS = {
                                    _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_verify_select": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i32, _i32, _c_void_p,
                                   _c_void_p, _c_void_p]),
+    "lopa_verify_select_ex": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i32, _f32,
+                                     _c_void_p, _c_void_p, _c_void_p]),
     "lopa_step": (_i32, [ctypes.POINTER(StepArgs), _c_void_p]),
     "lopa_bp_record_bytes": (_size, [_i32, _i32]),
     "lopa_bp_local": (_i32, [ctypes.POINTER(StepArgs), _i32, _i32, _c_void_p, _c_void_p]),
@@ -203,18 +209,24 @@ def spawn_branches(conf, argmax, tokens_b0, mask_b0, k: int):
 
 
 # ----------------------------------------------------------------------------- a2
-def verify_select(conf, branch_mask, n_branches):
-    """Eq. 2 + select.  conf/branch_mask [max_br][W]; n_branches device
-    int32[1].  Returns (scores f32[max_br], winner i32[1])."""
+def verify_select(conf, branch_mask, n_branches, metric: int = METRIC_MEAN, param: float = 0.0):
+    """Eq. 2 (or a P:204 variant) + select (P:198-204, P:176).  conf/branch_mask [max_br][W];
+    n_branches device int32[1].  Returns (scores f32[max_br], winner i32[1])."""
     _need_cuda(conf, branch_mask, n_branches)
     max_br, W = branch_mask.shape
     dev = branch_mask.device
     scores = torch.empty(max_br, dtype=torch.float32, device=dev)
     winner = torch.zeros(1, dtype=torch.int32, device=dev)
-    _check(lib().lopa_verify_select(_p(conf.contiguous()), _p(_u8(branch_mask).contiguous()),
-                                    _p(n_branches), max_br, W, _p(scores), _p(winner),
-                                    _stream(dev)),
-           "lopa_verify_select")
+    if metric == METRIC_MEAN:
+        _check(lib().lopa_verify_select(_p(conf.contiguous()), _p(_u8(branch_mask).contiguous()),
+                                        _p(n_branches), max_br, W, _p(scores), _p(winner),
+                                        _stream(dev)),
+               "lopa_verify_select")
+    else:
+        _check(lib().lopa_verify_select_ex(_p(conf.contiguous()), _p(_u8(branch_mask).contiguous()),
+                                           _p(n_branches), max_br, W, metric, param, _p(scores),
+                                           _p(winner), _stream(dev)),
+               "lopa_verify_select_ex")
     return scores, winner
 
 
@@ -237,8 +249,9 @@ class Stepper:
     configuration, so that repeated steps allocate nothing (CUDA-graph friendly)."""
 
     def __init__(self, vocab: int, window: int, max_branches: int, k: int, tau: float, device,
-                 ld: int | None = None):
+                 ld: int | None = None, metric: int = METRIC_MEAN, metric_param: float = 0.0):
         self.vocab, self.window, self.max_branches, self.k, self.tau = vocab, window, max_branches, k, tau
+        self.metric, self.metric_param = metric, metric_param
         self.ld = ld if ld is not None else ((vocab + 7) // 8) * 8
         self.device = torch.device(device)
         d = self.device
@@ -266,7 +279,7 @@ class Stepper:
             next_tokens=o.next_tokens.data_ptr(), next_mask=o.next_mask.data_ptr(),
             lookahead_pos=o.lookahead.data_ptr(), n_branches_next=o.n_next.data_ptr(),
             dev_status=o.status.data_ptr(), workspace=self.ws.data_ptr(),
-            workspace_bytes=self.ws.numel())
+            workspace_bytes=self.ws.numel(), metric=self.metric, metric_param=self.metric_param)
 
     def _validate(self, logits, n_branches, branch_tokens, branch_mask):
         _need_cuda(logits, n_branches, branch_tokens, branch_mask)

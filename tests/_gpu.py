@@ -49,12 +49,13 @@ def decision_gaps(conf_w, mask_w, anchor_mask, k, tau, scores):
     return gaps
 
 
-def check_step(out, logits_u16, tok, msk, n_br, k, tau, exempt_counter=None, vocab=None):
+def check_step(out, logits_u16, tok, msk, n_br, k, tau, exempt_counter=None, vocab=None,
+               metric=0, param=0.0):
     """Compare one fused-step output with the oracle on the same inputs.  Returns the oracle
     StepResult.  tok/msk: numpy [max_br][W]; logits_u16: numpy [>=n_br][W][ld]."""
     W = msk.shape[1]
     V_rows = logits_u16[:n_br, :, :vocab] if vocab else logits_u16[:n_br]   # the oracle reads V entries, not ld
-    ref = O.step(V_rows, tok[:n_br], msk[:n_br], k, tau)
+    ref = O.step(V_rows, tok[:n_br], msk[:n_br], k, tau, metric, param)
     g_conf = out.conf.cpu().numpy()[:n_br].astype(np.float64)
     g_amax = out.argmax.cpu().numpy()[:n_br].astype(np.int64)
     g_scores = out.scores.cpu().numpy()[:n_br].astype(np.float64)
@@ -73,7 +74,9 @@ def check_step(out, logits_u16, tok, msk, n_br, k, tau, exempt_counter=None, voc
     # a2: scores within tolerance
     assert np.max(np.abs(g_scores - np.array(ref.scores)), initial=0.0) <= CONF_TOL
     # decisions: exactly the oracle's decisions on the GPU's own fp32 values
-    cs = [O.branch_score(np.where(sel, g_conf, np.nan)[j], msk[j]) for j in range(n_br)]
+    cs = [O.branch_score(np.where(sel, g_conf, np.nan)[j], msk[j], metric, param) for j in range(n_br)]
+    # exact fp64 sums on both sides: the GPU score is the oracle's value (on GPU conf) rounded once
+    assert [float(np.float32(x)) for x in cs] == [float(x) for x in g_scores]
     # fp32-rounded score ties -> lowest index (the GPU selects on its fp32 scores)
     gs32 = [float(np.float32(x)) for x in cs]
     assert g_w == O.verify_select(gs32)

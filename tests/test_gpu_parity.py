@@ -234,8 +234,8 @@ def test_decisions_random_maps(L, W):
 
 
 # ----------------------------------------------------------------------------- fused step
-def _run_steps(L, seed, V, W, k, tau, iters, extras, blk=0, counter=None):
-    st = L.Stepper(V, W, k + 1, k, tau, DEV)
+def _run_steps(L, seed, V, W, k, tau, iters, extras, blk=0, counter=None, metric=0, param=0.0):
+    st = L.Stepper(V, W, k + 1, k, tau, DEV, metric=metric, metric_param=param)
     tok, msk, nb = G.fresh_tables(k, W, DEV)
     fills = 0
     for it in range(iters):
@@ -244,7 +244,8 @@ def _run_steps(L, seed, V, W, k, tau, iters, extras, blk=0, counter=None):
         L.syn_generate(seed, blk, V, tok, msk, n_branches=n, extras=extras, out=logits[:n])
         out = st.step(logits, nb, tok, msk)
         torch.cuda.synchronize()
-        G.check_step(out, G.to_np_u16(logits), tok.cpu().numpy(), msk.cpu().numpy(), n, k, tau, counter, vocab=V)
+        G.check_step(out, G.to_np_u16(logits), tok.cpu().numpy(), msk.cpu().numpy(), n, k, tau, counter,
+                     vocab=V, metric=metric, param=param)
         if int(out.n_next.item()) == 0:
             return it + 1
         tok, msk, nb = out.next_tokens.clone(), out.next_mask.clone(), out.n_next.clone()
@@ -464,3 +465,44 @@ def test_dense_rows_roofline_mode(L):
     for r in (0, 77, 128, 255):
         rc, ra, _ = O.row_confidence(xs[r])
         assert abs(c[r].item() - rc) <= 2e-6 and a[r].item() == ra
+
+
+# ----------------------------------------------------------------------------- Eq. 2 variants
+def test_spec_sliding_window_on_gpu(L):
+    """[.9,.2,.8] in position order, sliding_window(2) -> 0.5."""
+    conf = torch.tensor([[0.9, 0.2, 0.8]], dtype=torch.float32, device=DEV)
+    mask = torch.ones((1, 3), dtype=torch.uint8, device=DEV)
+    s, w = L.verify_select(conf, mask, torch.ones(1, dtype=torch.int32, device=DEV),
+                           metric=L.METRIC_SLIDING_MIN, param=2.0)
+    assert s.item() == float(np.float32(O.branch_score(conf.cpu().numpy()[0].astype(np.float64), [1, 1, 1],
+                                                       O.METRIC_SLIDING_MIN, 2)))
+    assert abs(s.item() - 0.5) < 1e-7
+
+
+@pytest.mark.parametrize("metric,param", [(1, 1.0), (1, 3.0), (1, 64.0), (2, 0.25), (2, 0.5), (2, 1.0),
+                                          (2, 0.1)])
+def test_metric_variants_random_maps(L, metric, param):
+    """The P:204 variants on random confidence maps with forced ties: scores bit-equal to the
+    oracle's fp64 value rounded to fp32 (exact sums on both sides); winner by the oracle's rule."""
+    rng = np.random.default_rng(int(metric * 100 + param * 10))
+    for it in range(40):
+        W = int(rng.integers(1, 65))
+        nbr = int(rng.integers(1, 33))
+        bc = rng.random((nbr, W)).astype(np.float32)
+        if it % 3 == 0:
+            bc = rng.choice(np.float32([0.25, 0.5, 0.75]), size=(nbr, W))
+        bm = (rng.random((nbr, W)) < 0.6).astype(np.uint8)
+        s, w = L.verify_select(torch.from_numpy(bc).to(DEV), torch.from_numpy(bm).to(DEV),
+                               torch.tensor([nbr], dtype=torch.int32, device=DEV), metric=metric, param=param)
+        rs = [O.branch_score(bc[j].astype(np.float64), bm[j], metric, param) for j in range(nbr)]
+        rs32 = [float(np.float32(x)) for x in rs]
+        assert s.cpu().tolist() == rs32
+        assert int(w.item()) == O.verify_select(rs32)
+
+
+@pytest.mark.parametrize("metric,param", [(1, 4.0), (2, 0.3)])
+def test_step_with_metric_variants(L, metric, param):
+    """Full fused steps with a P:204 branch-confidence variant: toy (iterated) and Dream shape."""
+    for seed in range(20):
+        _run_steps(L, seed, 64, 8, 2, 0.9, 20, extras=1, metric=metric, param=param)
+    _run_steps(L, 1, 151936, 32, 7, 0.9, 2, extras=0, metric=metric, param=param)
