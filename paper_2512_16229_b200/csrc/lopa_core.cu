@@ -100,7 +100,7 @@ struct Params {
   float* conf;
   int32_t* argmax;
   int32_t* dev_status;
-  uint32_t* ctrs;              // [0] work-item counter, [2] n_masked (K1 -> K2)
+  uint32_t* ctrs;              // [0] work-item counter
   float4* gpart;               // [n_grp][n_cand] group partials (m, s, argmax bits, -), group-major
   int mode;
   // tails
@@ -571,8 +571,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   uint32_t* icnt = reinterpret_cast<uint32_t*>(ipart + kItemSlots * kPartPerItem);
   uint32_t* gbits = icnt + kItemSlots;
   uint32_t* goff = gbits + kMaxGroups;
-  uint32_t* misc = goff + kMaxGroups;  // [0] = n_masked, [1] = last-CTA flag
-  uint16_t* row_list = reinterpret_cast<uint16_t*>(misc + 4);
+  uint32_t* misc = goff + kMaxGroups;  // [0] = rows of present branches
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) TL(0);
@@ -590,12 +589,42 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   // global inputs, then let the dependent fold/tail kernel launch (it may prefetch the inputs).
   grid_dep_wait();
   grid_dep_launch();
-  // ---- in-kernel row compaction: rows with mask = 1 of present branches
+  // ---- work items live in the raw row space: item = row * n_grp + group.  Rows that are not
+  // masked (or belong to absent branches) are skipped; no compaction pass is needed, so the
+  // producer issues its first bulk copy before the masks have even arrived (speculatively: a
+  // copy of a row that turns out invalid is discarded by the consumers).
   const int W = P.window;
+  const int n_seg = P.n_seg, n_grp = P.n_grp;
+  const int G = (int)gridDim.x;
+  const int n_items_cap = P.n_cand * n_grp;
+  const uint64_t pol = policy_evict_first();
+  uint32_t i = 0;  // producer: item (= stage use) sequence number of this CTA
+  // Issue one work item (raw row, group g): ONE bulk copy of its <= kSegPerItem segments.
+  auto issue = [&](int cur) {
+    const int row = cur / n_grp, g = cur - row * n_grp;
+    const int s0 = g * kSegPerItem, s1 = min(n_seg, s0 + kSegPerItem);
+    const int slot = (int)(i % kItemSlots);
+    if (i >= (uint32_t)kItemSlots) mbar_wait(&slot_free[slot], ((i / kItemSlots) - 1) & 1);
+    const int s = (int)(i % kStages);
+    if (i >= (uint32_t)kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+    stage_info[s] = make_int4(row, g, slot, s1 - s0);
+    const int e0 = s0 * P.seg_len;
+    const int e1 = min(P.vocab, s1 * P.seg_len);
+    const uint32_t bytes = (uint32_t)(((e1 - e0 + 7) >> 3) << 4);
+    mbar_arrive_expect_tx(&full[s], bytes);
+    bulk_g2s(stages + (size_t)s * kStageBytes, P.logits + (size_t)row * P.ld + e0, bytes,
+             &full[s], pol);
+    ++i;
+  };
+  const int b = blockIdx.x;
+  if (tid == 0) {
+    TL(1);
+    if (b < n_items_cap) issue(b);  // speculative: validity is checked by the consumers
+  }
+  // valid-row bits: mask byte and n_branches loaded independently (one round trip)
   const int n_groups = (P.n_cand + 31) >> 5;
   for (int g = warp; g < n_groups; g += kWarps) {
     const int r = g * 32 + lane;
-    // the mask byte and n_branches are loaded independently (one round trip)
     const bool in = r < P.n_cand;
     const bool mk = (in && P.row_mask) ? P.row_mask[r] != 0 : in;
     const int nb_eff = P.n_branches ? *P.n_branches - P.branch_base : 0x7FFFFFFF;
@@ -603,90 +632,35 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     if (v && P.n_branches) v = (r / W) < nb_eff;
     const uint32_t bits = __ballot_sync(0xffffffffu, v);
     if (lane == 0) gbits[g] = bits;
+    if (g == 0 && lane == 0)
+      misc[0] = P.n_branches ? (uint32_t)max(0, min(nb_eff, P.n_cand / W)) * W : (uint32_t)P.n_cand;
   }
   __syncthreads();
-  if (warp == 0) {
-    // exclusive scan of group popcounts: lane owns groups 4 lane .. 4 lane + 3
-    uint32_t c[4], tot = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int g = 4 * lane + q;
-      c[q] = g < n_groups ? __popc(gbits[g]) : 0u;
-      tot += c[q];
-    }
-    uint32_t incl = tot;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += y;
-    }
-    uint32_t run = incl - tot;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int g = 4 * lane + q;
-      if (g < n_groups) goff[g] = run;
-      run += c[q];
-    }
-    if (lane == 31) misc[0] = incl;
-  }
-  __syncthreads();
-  for (int g = warp; g < n_groups; g += kWarps) {
-    const uint32_t bits = gbits[g];
-    if ((bits >> lane) & 1u)
-      row_list[goff[g] + __popc(bits & ((1u << lane) - 1u))] = (uint16_t)(g * 32 + lane);
-  }
-  __syncthreads();
-
-  const int n_masked = (int)misc[0];
-  const int n_seg = P.n_seg, n_grp = P.n_grp;
-  const int n_items = n_masked * n_grp;
-  const int G = (int)gridDim.x;
+  auto row_valid = [&](int r) -> bool { return (gbits[r >> 5] >> (r & 31)) & 1u; };
+  const int n_items = (int)misc[0] * n_grp;  // items of present branches' rows
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---- TMA producer: items blockIdx.x, then G + counter, ...
-      const uint64_t pol = policy_evict_first();
-      TL(1);
-      uint32_t i = 0;  // item (= stage use) sequence number of this CTA
-      // Issue one work item (row rc, group g): ONE bulk copy of its <= kSegPerItem segments.
-      auto issue = [&](int cur) {
-        const int rc = cur / n_grp, g = cur - rc * n_grp;
-        const int row = row_list[rc];
-        const int s0 = g * kSegPerItem, s1 = min(n_seg, s0 + kSegPerItem);
-        const int slot = (int)(i % kItemSlots);
-        if (i >= (uint32_t)kItemSlots) mbar_wait(&slot_free[slot], ((i / kItemSlots) - 1) & 1);
-        const int s = (int)(i % kStages);
-        if (i >= (uint32_t)kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
-        stage_info[s] = make_int4(rc, g, slot, s1 - s0);
-        const int e0 = s0 * P.seg_len;
-        const int e1 = min(P.vocab, s1 * P.seg_len);
-        const uint32_t bytes = (uint32_t)(((e1 - e0 + 7) >> 3) << 4);
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(stages + (size_t)s * kStageBytes, P.logits + (size_t)row * P.ld + e0, bytes,
-                 &full[s], pol);
-        ++i;
+      // ---- TMA producer: items b (issued above), G + b, then 2G + counter, ...  Claims on
+      // unmasked rows are skipped without a copy; two claims stay in flight so the atomic's
+      // latency hides behind the issue of two items.
+      const bool dyn = 2 * G < n_items;
+      uint32_t p1 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
+      uint32_t p2 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
+      auto maybe_issue = [&](int cur) {
+        if (row_valid(cur / n_grp)) issue(cur);
       };
-      // Items blockIdx.x and G + blockIdx.x are static; later items come from the counter
-      // (numbered from 2G), with two claims in flight so the atomic's latency stays hidden
-      // behind the issue of two items.
-      const int b = blockIdx.x;
-      if (b < n_items) {
-        const bool dyn = 2 * G < n_items;
-        uint32_t p1 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
-        uint32_t p2 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
-        issue(b);
-        if (G + b < n_items) issue(G + b);
-        if (dyn) {
-          while (true) {
-            const int c1 = 2 * G + (int)p1;
-            if (c1 >= n_items) break;
-            p1 = atomicAdd(&P.ctrs[0], 1u);
-            issue(c1);
-            const int c2 = 2 * G + (int)p2;
-            if (c2 >= n_items) break;
-            p2 = atomicAdd(&P.ctrs[0], 1u);
-            issue(c2);
-          }
+      if (G + b < n_items) maybe_issue(G + b);
+      if (dyn) {
+        while (true) {
+          const int c1 = 2 * G + (int)p1;
+          if (c1 >= n_items) break;
+          p1 = atomicAdd(&P.ctrs[0], 1u);
+          maybe_issue(c1);
+          const int c2 = 2 * G + (int)p2;
+          if (c2 >= n_items) break;
+          p2 = atomicAdd(&P.ctrs[0], 1u);
+          maybe_issue(c2);
         }
       }
       // end-of-work sentinels: one stage per consumer phase (every warpgroup sees one)
@@ -712,8 +686,9 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
       first = false;
       const int4 info = stage_info[s];
       if (info.x < 0) break;
-      const int rc = info.x, g = info.y, slot = info.z, nsi = info.w;
-      if (jseg >= nsi) {  // short item (last group of a row): nothing for this warpgroup
+      const int row = info.x, g = info.y, slot = info.z, nsi = info.w;
+      if (jseg >= nsi || !row_valid(row)) {  // short item, or a speculative copy of a skipped row
+        if (jseg == 0 && wq == 0 && lane == 0 && !row_valid(row)) mbar_arrive(&slot_free[slot]);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         continue;
@@ -735,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
           __threadfence_block();
           const float4* q = ipart + slot * kPartPerItem;
           const FoldAcc f = fold_seq(kWarpsPerSeg * nsi, [&](int p) { return q[p]; });
-          P.gpart[(size_t)g * P.n_cand + row_list[rc]] = make_float4(f.M, f.S, __uint_as_float(f.a), 0.f);
+          P.gpart[(size_t)g * P.n_cand + row] = make_float4(f.M, f.S, __uint_as_float(f.a), 0.f);
           icnt[slot] = 0;
           mbar_arrive(&slot_free[slot]);
         }
@@ -872,7 +847,7 @@ static_assert(4 * kTailThreads >= LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW, "4 table 
 
 constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + (2 * kStages + kItemSlots) * 8 +
                               kStages * 16 + kItemSlots * kPartPerItem * 16 + kItemSlots * 4 +
-                              2 * kMaxGroups * 4 + 16 + LOPA_MAX_ROWS * 2;
+                              2 * kMaxGroups * 4 + 16;
 
 // ------------------------------------------------------------------ small decision kernels
 __global__ void anchor_kernel(const float* conf, const int32_t* argmax, const int32_t* tokens,
