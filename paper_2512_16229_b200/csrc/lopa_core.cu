@@ -63,7 +63,7 @@ __device__ __forceinline__ void tl_clk(int slot) { g_timeline[blockIdx.x * kTlSl
 namespace lopa {
 
 #ifndef LOPA_STAGES
-#define LOPA_STAGES 6
+#define LOPA_STAGES 3
 #endif
 #ifndef LOPA_WGS
 #define LOPA_WGS 6
@@ -726,7 +726,10 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
 // One CTA, launched programmatically dependent on K1: its launch and prologue overlap K1, and
 // griddepcontrol.wait returns once K1's writes are visible.  It folds every masked row's group
 // partials in fixed order (conf bits depend only on the row's bytes) and runs the tail.
-constexpr int kTailThreads = 512;
+#ifndef LOPA_TAIL_THREADS
+#define LOPA_TAIL_THREADS 512
+#endif
+constexpr int kTailThreads = LOPA_TAIL_THREADS;
 constexpr size_t kTailSmemBytes = kTailBytes + LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW * 2;
 
 
