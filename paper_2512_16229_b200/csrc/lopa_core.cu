@@ -1093,7 +1093,7 @@ static int launch_reduce(const Params& P, int device, cudaStream_t s) {
   if (st != LOPA_OK) return st;
   // One SM is left to the fold/tail kernel: it becomes resident there while K1 streams (PDL)
   // and, landing on the same SM step after step, runs with a warm instruction cache.
-  const int grid = LOPA_CTAS_PER_SM * num_sms(device) - (P.mode == MODE_CONF ? 0 : 1);
+  const int grid = LOPA_CTAS_PER_SM * (num_sms(device) - (P.mode == MODE_CONF ? 0 : 1));
   if (grid <= 0) return LOPA_ERR_CUDA;
   int pslot = -1;
   prof_record(0, s, &pslot);
