@@ -34,6 +34,16 @@ import torch  # noqa: E402
 METRIC = "LoPA verify-steps/s and logits HBM GB/s (V=151936,k+1 branches) at 1/2/4/8 B200"
 UNIT = "verify-steps/s"
 CFG = dict(V=151936, W=32, k=7, tau=0.9, seed=1, n_buf=8)
+# other BASELINE.json configs, selectable with --config (the headline is configs[1] = "dream")
+CONFIGS = {
+    "dream": dict(V=151936, W=32, k=7, tau=0.9, name="D2F-Dream verify step V=151936 W=32 k=7 tau=0.9 (configs[1])"),
+    "dream-k15": dict(V=151936, W=32, k=15, tau=0.9, name="D2F-Dream verify step V=151936 W=32 k=15 tau=0.9 (configs[2] shape)"),
+    "diffucoder": dict(V=151936, W=32, k=10, tau=0.95, name="D2F-DiffuCoder verify step V=151936 W=32 k=10 tau=0.95 (configs[3] shape)"),
+}
+for _k in (1, 3, 7, 15, 31):
+    for _w in (16, 32, 64):
+        CONFIGS[f"sweep-k{_k}-w{_w}"] = dict(V=151936, W=_w, k=_k, tau=0.9,
+                                             name=f"sweep V=151936 W={_w} k={_k} tau=0.9 (configs[4])")
 
 
 def peaks():
@@ -197,7 +207,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SYN-D2F seeded logits; no weights)",
-            "config": {"workload": "D2F-Dream verify step V=151936 W=32 k=7 tau=0.9 (configs[1])",
+            "config": {"workload": CFG.get("name", "D2F-Dream verify step V=151936 W=32 k=7 tau=0.9 (configs[1])"),
                        "masked_rows": len(rows), "sampled_rows_per_step": n_s},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{n_s} of {len(rows)} masked rows per step (+ full a2-a4), "
@@ -359,7 +369,7 @@ def run_lopa(args):
             "warmup": args.warmup, "ms_per_step": el_ms / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (SYN-D2F seeded logits; transformer forward out of scope)",
-            "config": {"workload": "D2F-Dream verify step V=151936 W=32 k=7 tau=0.9 (configs[1])",
+            "config": {"workload": CFG.get("name", "D2F-Dream verify step V=151936 W=32 k=7 tau=0.9 (configs[1])"),
                        "branches": int(nb.item()), "masked_rows": rows_total,
                        "masked_rows_this_rank": rows_local,
                        "parallelism": f"bp{world}" if world > 1 else "single",
@@ -393,7 +403,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="lopa", choices=["lopa", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="dream", choices=sorted(CONFIGS))
     args = ap.parse_args()
+    c = CONFIGS[args.config]
+    CFG.update(V=c["V"], W=c["W"], k=c["k"], tau=c["tau"], name=c["name"])
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -155,6 +155,9 @@ __host__ __device__ inline RecordView record_view(void* base, int32_t b_loc) {
 
 // Programmatic dependent launch (PDL): the next kernel in the stream may launch early; its
 // griddepcontrol.wait returns once this grid's memory operations are visible.
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
 
@@ -453,6 +456,9 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
   cta_scores<NT>(T, P, nb, W, warp, lane, P.scores);
   __syncthreads();
   TL(7);
+  // the rest runs on warps 0-1 only (64 threads = one per window position), synchronised with a
+  // 64-thread named barrier instead of CTA-wide barriers
+  if (warp >= 2) return;
   if (warp == 0) {
     const float sc = lane < P.cap ? T.scores[lane] : -INFINITY;
     const int w = warp_select(sc, lane, nb);
@@ -483,45 +489,46 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
       T.n = any ? min(P.k, n_mb0) : -1;
     }
   }
-  __syncthreads();
+  named_bar_sync(1, 64);
   TL(9);
   const int nl = T.n;
   if (nl < 0) {  // R21: the winner is complete -> pass it through, no branches
-    for (int i = tid; i < W; i += NT) {
-      P.next_tokens[i] = T.b0_tok[i];
-      P.next_mask[i] = T.b0_msk[i];
+    if (tid < W) {
+      P.next_tokens[tid] = T.b0_tok[tid];
+      P.next_mask[tid] = T.b0_msk[tid];
     }
     if (P.lookahead)
-      for (int q = tid; q < P.k; q += NT) P.lookahead[q] = -1;
+      for (int q = tid; q < P.k; q += 64) P.lookahead[q] = -1;
     if (tid == 0) *P.n_next = 0;
     return;
   }
-  // Alg. 1 step 2: rank of each position of M_B0 under (conf desc, position asc)
-  // (4 threads per position, 16 keys each, combined with two shuffles)
-  if (tid < 4 * LOPA_MAX_WINDOW) {
-    const int pos = tid >> 2, part = tid & 3;
+  // Alg. 1 step 2: rank of each position of M_B0 under (conf desc, position asc), one thread
+  // per position counting the larger keys (broadcast shared-memory reads)
+  {
+    const int pos = tid;
     const uint64_t mine = T.keys[pos];
     int cnt = 0;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) cnt += (T.keys[16 * part + q] > mine) ? 1 : 0;
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
-    if (part == 0) {
-      const int rk = T.b0_msk[pos] ? cnt : (1 << 20);
-      T.rank[pos] = rk;
-      if (rk < nl && P.lookahead) P.lookahead[rk] = pos;
-    }
+#pragma unroll 16
+    for (int q = 0; q < LOPA_MAX_WINDOW; ++q) cnt += (T.keys[q] > mine) ? 1 : 0;
+    const int rk = T.b0_msk[pos] ? cnt : (1 << 20);
+    T.rank[pos] = rk;
+    if (rk < nl && P.lookahead) P.lookahead[rk] = pos;
+    if (P.lookahead)
+      for (int q = nl + tid; q < P.k; q += 64) P.lookahead[q] = -1;
   }
-  if (P.lookahead)
-    for (int q = nl + tid; q < P.k; q += NT) P.lookahead[q] = -1;
-  __syncthreads();
+  named_bar_sync(1, 64);
   TL(12);
-  const int total = (nl + 1) * W;
-  for (int idx = tid; idx < total; idx += NT) {
-    const int j = idx / W, i = idx - j * W;
-    const bool fill = (j >= 1) && (T.rank[i] == j - 1);
-    P.next_tokens[idx] = fill ? T.b0_amax[i] : T.b0_tok[i];
-    P.next_mask[idx] = fill ? (uint8_t)0 : T.b0_msk[i];
+  // next tables: thread = position i, rows j = 0..nl
+  if (tid < W) {
+    const int i = tid;
+    const int32_t tb = T.b0_tok[i], ta = T.b0_amax[i];
+    const uint8_t mb = T.b0_msk[i];
+    const int rk = T.rank[i];
+    for (int j = 0; j <= nl; ++j) {
+      const bool fill = (j >= 1) && (rk == j - 1);
+      P.next_tokens[(size_t)j * W + i] = fill ? ta : tb;
+      P.next_mask[(size_t)j * W + i] = fill ? (uint8_t)0 : mb;
+    }
   }
   if (tid == 0) *P.n_next = nl + 1;
   TL(13);
