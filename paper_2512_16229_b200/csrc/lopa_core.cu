@@ -255,11 +255,21 @@ __device__ __forceinline__ Partial reduce_slice(const uint8_t* stage, int nchunk
                                                 int vocab, int wq, int lane, uint64_t* empty_bar) {
   const uint4* buf = reinterpret_cast<const uint4*>(stage);
   uint4 v[kChunksPerLane];
+  if (nchunks >= 128 * (kChunksPerLane - 1)) {
+    // common case (a full-size segment): only the last chunk of a lane can fall outside
 #pragma unroll
-  for (int t = 0; t < kChunksPerLane; ++t) {
-    const int c = 128 * t + 32 * wq + lane;
-    v[t] = (c < nchunks) ? lds128(buf + c)
-                         : make_uint4(kNegInfBf16x2, kNegInfBf16x2, kNegInfBf16x2, kNegInfBf16x2);
+    for (int t = 0; t < kChunksPerLane - 1; ++t) v[t] = lds128(buf + 128 * t + 32 * wq + lane);
+    const int c = 128 * (kChunksPerLane - 1) + 32 * wq + lane;
+    v[kChunksPerLane - 1] = lds128(buf + min(c, nchunks - 1));
+    if (c >= nchunks)
+      v[kChunksPerLane - 1] = make_uint4(kNegInfBf16x2, kNegInfBf16x2, kNegInfBf16x2, kNegInfBf16x2);
+  } else {
+#pragma unroll
+    for (int t = 0; t < kChunksPerLane; ++t) {
+      const int c = 128 * t + 32 * wq + lane;
+      v[t] = (c < nchunks) ? lds128(buf + c)
+                           : make_uint4(kNegInfBf16x2, kNegInfBf16x2, kNegInfBf16x2, kNegInfBf16x2);
+    }
   }
 #ifdef LOPA_NOCOMPUTE
   // streaming experiment: consume the stage and return a dummy partial

@@ -11,6 +11,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // ---- mbarrier ----------------------------------------------------------------------------
+// try_wait suspend-time hint: a waiting warp sleeps in hardware until the phase completes (or
+// the hint expires) instead of spinning and stealing issue slots from the computing warps.
+#ifndef LOPA_MBAR_SUSPEND_NS
+#define LOPA_MBAR_SUSPEND_NS 0x989680
+#endif
+constexpr uint32_t kMbarSuspendNs = LOPA_MBAR_SUSPEND_NS;  // default 10 ms
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
                : "memory");
@@ -37,10 +43,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred p;\n"
       "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra LAB_WAIT;\n"
       "}\n" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(kMbarSuspendNs)
       : "memory");
 }
 
