@@ -70,9 +70,9 @@ typedef enum {
 #define LOPA_DEV_NONFINITE 2  /* a reduced row holds NaN or +inf, or is all -inf (R20);
                                  that row's conf / argmax are unspecified                   */
 
-#define LOPA_MAX_WINDOW 64    /* W <= 64: one warp owns a window (NEXT-1 lifts this)        */
+#define LOPA_MAX_WINDOW 256   /* W <= 256 (the D2F multi-block window); W > 64 needs V <= 2^22 */
 #define LOPA_MAX_BRANCHES 32  /* k + 1 <= 32: one lane per branch in the select             */
-#define LOPA_MAX_ROWS 4096    /* rows per lopa_confidence call                              */
+#define LOPA_MAX_ROWS 4096    /* rows per call: n_rows, or max_branches * window            */
 #define LOPA_MAX_VOCAB (1 << 23) /* conf >= 1/V >= 2^-23 keeps the fp64 Eq. 2 sums exact       */
 
 int lopa_version(void);
@@ -106,6 +106,13 @@ int lopa_confidence(const void* logits, int64_t ld, int32_t n_rows, int32_t voca
 int lopa_anchor_fill(const float* conf, const int32_t* argmax, const int32_t* tokens,
                      const uint8_t* mask, int32_t window, float tau, int32_t* tokens_out,
                      uint8_t* mask_out, int32_t* dev_status, void* stream);
+
+/* a3 with per-position thresholds (the D2F multi-block window; R25):
+ * tau_pos device float [window] or NULL (NULL = tau everywhere). */
+int lopa_anchor_fill_ex(const float* conf, const int32_t* argmax, const int32_t* tokens,
+                        const uint8_t* mask, int32_t window, float tau, const float* tau_pos,
+                        int32_t* tokens_out, uint8_t* mask_out, int32_t* dev_status,
+                        void* stream);
 
 /* a4 — Alg. 1 step 2.
  *   conf, argmax        device [window] (the anchor's confidences, read where mask_b0 == 1)
@@ -173,6 +180,8 @@ typedef struct {
   size_t workspace_bytes;        /* >= lopa_workspace_bytes(max_branches * window, vocab)   */
   int32_t metric;                /* branch confidence: LOPA_METRIC_* (0 = Eq. 2 mean)        */
   float metric_param;            /* window w >= 1 (integer) or eta in (0, 1]; unused for mean */
+  const float* tau_pos;          /* device float [window] per-position Eq. 1 thresholds, or
+                                    NULL (= tau): the D2F window's tau_act / tau_conf         */
 } lopa_step_args_t;
 
 /* Next tables must not alias the input tables.  Errors: INVALID_ARG, UNSUPPORTED, CUDA. */

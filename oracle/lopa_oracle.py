@@ -104,12 +104,17 @@ class FillDecision:
 
 
 def select_fill_set(conf, mask, tau) -> FillDecision:
-    """Eq. 1 on the positions i with mask[i] = 1."""
-    t = tau_as_f64(tau)
+    """Eq. 1 on the positions i with mask[i] = 1.
+
+    ``tau`` is a scalar or, for the D2F multi-block window (reading R25), one
+    threshold per window position (tau_act on the newest active block, tau_conf on older ones)."""
+    taus = np.atleast_1d(np.asarray(tau, dtype=np.float64))
     M = [i for i in range(len(mask)) if mask[i]]
     if not M:
         raise EmptyMaskError("Eq. 1 with an empty masked set")
-    s_high = [i for i in M if float(conf[i]) > t]
+    def t_at(i):
+        return tau_as_f64(taus[i] if taus.size > 1 else taus[0])
+    s_high = [i for i in M if float(conf[i]) > t_at(i)]
     if s_high:
         return FillDecision(s_high, list(s_high), False)
     best = max(float(conf[i]) for i in M)

@@ -108,6 +108,7 @@ struct Params {
   const uint8_t* branch_mask;
   int32_t k;
   float tau;
+  const float* tau_pos;        // nullable: per-position Eq. 1 thresholds of the window (D2F)
   int32_t metric;              // branch-confidence metric (kMetric*)
   float metric_param;          // window w (sliding) or eta (bottom fraction)
   float* scores;
@@ -421,11 +422,12 @@ __device__ __forceinline__ FoldAcc fold_tree16(int n, const float4 (&q)[16]) {
 
 // ------------------------------------------------------------------ last-CTA tail
 // Everything the decision tail needs, staged in the (idle) TMA ring of the last CTA.
+constexpr int kScoreWarps = 8;  // warps scoring branches in the tail
 struct TailSmem {
-  float conf[LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW];
-  int32_t amax[LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW];
-  int32_t tok[LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW];
-  uint8_t msk[LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW];
+  float conf[LOPA_MAX_ROWS];
+  int32_t amax[LOPA_MAX_ROWS];
+  int32_t tok[LOPA_MAX_ROWS];
+  uint8_t msk[LOPA_MAX_ROWS];
   float scores[LOPA_MAX_BRANCHES];
   uint64_t keys[LOPA_MAX_WINDOW];
   int32_t b0_tok[LOPA_MAX_WINDOW];
@@ -434,22 +436,23 @@ struct TailSmem {
   int32_t rank[LOPA_MAX_WINDOW];
   int32_t n;       // lookahead count, -1 = winner complete
   int32_t best;    // (BP) local best
-  double dscr[16][LOPA_MAX_WINDOW];  // per-warp metric scratch (warps 0..15)
-  float fscr[16][LOPA_MAX_WINDOW];
+  double dscr[kScoreWarps][LOPA_MAX_WINDOW];  // per-warp metric scratch
+  float fscr[kScoreWarps][LOPA_MAX_WINDOW];
 };
 constexpr size_t kTailBytes = (sizeof(TailSmem) + 127) / 128 * 128;
 
 // Eq. 2 (or a variant) for branches [0, cap) of the staged table (nb present): warp w
 // scores branches w, w + NT/32, ... (warp_metric_score: exact fp64 sums).
-template <int NT>
+template <int NT, int S>
 __device__ __forceinline__ void cta_scores(TailSmem& T, const Params& P, int nb, int W, int warp,
                                            int lane, float* out) {
-  static_assert(NT / 32 <= 16, "metric scratch holds 16 warps");
-  for (int j = warp; j < P.cap; j += NT / 32) {
+  static_assert(NT / 32 >= kScoreWarps, "scoring warps");
+  if (warp >= kScoreWarps) return;
+  for (int j = warp; j < P.cap; j += kScoreWarps) {
     float sc = -INFINITY;
     if (j < nb)
-      sc = warp_metric_score(T.conf + j * W, T.msk + j * W, W, P.metric, P.metric_param,
-                             T.dscr[warp], T.fscr[warp], lane);
+      sc = warp_metric_score<S>(T.conf + j * W, T.msk + j * W, W, P.metric, P.metric_param,
+                                T.dscr[warp], T.fscr[warp], lane);
     if (lane == 0) {
       T.scores[j] = sc;
       if (out) out[j] = sc;
@@ -457,24 +460,24 @@ __device__ __forceinline__ void cta_scores(TailSmem& T, const Params& P, int nb,
   }
 }
 
-// a2 -> a3 -> a4 with all NT threads of the tail CTA (T.conf / T.amax hold the folded rows).
-template <int NT>
+// a2 -> a3 -> a4 with the tail CTA (T.conf / T.amax hold the folded rows).  After the scores,
+// warps 0..S-1 (32 S threads = one per window position) finish with a named barrier.
+template <int NT, int S>
 __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
   const int warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
   const int nb = max(0, min(*P.n_branches, P.cap));
-  cta_scores<NT>(T, P, nb, W, warp, lane, P.scores);
+  cta_scores<NT, S>(T, P, nb, W, warp, lane, P.scores);
   __syncthreads();
   TL(7);
-  // the rest runs on warps 0-1 only (64 threads = one per window position), synchronised with a
-  // 64-thread named barrier instead of CTA-wide barriers
-  if (warp >= 2) return;
+  if (warp >= S) return;
+  constexpr int kPos = 32 * S;
   if (warp == 0) {
     const float sc = lane < P.cap ? T.scores[lane] : -INFINITY;
     const int w = warp_select(sc, lane, nb);
-    WinRegs r;
+    WinRegs<S> r;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < S; ++h) {
       const int i = lane + 32 * h;
       const bool in = i < W;
       r.msk[h] = in ? (uint32_t)T.msk[w * W + i] : 0u;
@@ -482,16 +485,20 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
       r.conf[h] = in ? T.conf[w * W + i] : 0.f;
       r.amax[h] = in ? T.amax[w * W + i] : -1;
     }
-    const bool any = __ballot_sync(0xffffffffu, r.msk[0] | r.msk[1]) != 0;
-    if (any) warp_anchor(r, P.tau, lane);
+    bool anym = false;
+#pragma unroll
+    for (int h = 0; h < S; ++h) anym |= r.msk[h] != 0;
+    const bool any = __any_sync(0xffffffffu, anym);
+    if (any) warp_anchor<S>(r, P.tau, P.tau_pos, W, lane);
     int n_mb0 = 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < S; ++h) {
       const int i = lane + 32 * h;
       T.b0_tok[i] = r.tok[h];
       T.b0_amax[i] = r.amax[h];
       T.b0_msk[i] = (uint8_t)r.msk[h];
-      T.keys[i] = r.msk[h] ? (((uint64_t)ordered_bits(r.conf[h]) << 32) | (uint64_t)(63 - i)) : 0ull;
+      T.keys[i] = r.msk[h] ? (((uint64_t)ordered_bits(r.conf[h]) << 32) | (uint64_t)(kPos - 1 - i))
+                           : 0ull;
       n_mb0 += __popc(__ballot_sync(0xffffffffu, r.msk[h]));
     }
     if (lane == 0) {
@@ -499,7 +506,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
       T.n = any ? min(P.k, n_mb0) : -1;
     }
   }
-  named_bar_sync(1, 64);
+  named_bar_sync(1, kPos);
   TL(9);
   const int nl = T.n;
   if (nl < 0) {  // R21: the winner is complete -> pass it through, no branches
@@ -508,7 +515,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
       P.next_mask[tid] = T.b0_msk[tid];
     }
     if (P.lookahead)
-      for (int q = tid; q < P.k; q += 64) P.lookahead[q] = -1;
+      for (int q = tid; q < P.k; q += kPos) P.lookahead[q] = -1;
     if (tid == 0) *P.n_next = 0;
     return;
   }
@@ -519,14 +526,14 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
     const uint64_t mine = T.keys[pos];
     int cnt = 0;
 #pragma unroll 16
-    for (int q = 0; q < LOPA_MAX_WINDOW; ++q) cnt += (T.keys[q] > mine) ? 1 : 0;
+    for (int q = 0; q < kPos; ++q) cnt += (T.keys[q] > mine) ? 1 : 0;
     const int rk = T.b0_msk[pos] ? cnt : (1 << 20);
     T.rank[pos] = rk;
     if (rk < nl && P.lookahead) P.lookahead[rk] = pos;
     if (P.lookahead)
-      for (int q = nl + tid; q < P.k; q += 64) P.lookahead[q] = -1;
+      for (int q = nl + tid; q < P.k; q += kPos) P.lookahead[q] = -1;
   }
-  named_bar_sync(1, 64);
+  named_bar_sync(1, kPos);
   TL(12);
   // next tables: thread = position i, rows j = 0..nl
   if (tid < W) {
@@ -546,13 +553,13 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
 
 // Local half of a BP step with all threads of the last CTA: local Eq. 2 scores, local best
 // (smallest local j with the largest score), and the exchange record.
-template <int NT>
+template <int NT, int S>
 __device__ void cta_tail_bp_local(const Params& P, TailSmem& T, int tid) {
   const int warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
   const int nb = max(0, min(*P.n_branches - P.branch_base, P.cap));
   RecordView rv = record_view(P.record, P.cap);
-  cta_scores<NT>(T, P, nb, W, warp, lane, rv.scores);
+  cta_scores<NT, S>(T, P, nb, W, warp, lane, rv.scores);
   __syncthreads();
   if (warp == 0) {
     const float sc = lane < P.cap ? T.scores[lane] : -INFINITY;
@@ -747,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
 #define LOPA_TAIL_THREADS 512
 #endif
 constexpr int kTailThreads = LOPA_TAIL_THREADS;
-constexpr size_t kTailSmemBytes = kTailBytes + LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW * 2;
+constexpr size_t kTailSmemBytes = kTailBytes + LOPA_MAX_ROWS * 2;
 
 
 // Fold one row's group partials (read straight from the group-major workspace: group g of row r
@@ -764,7 +771,7 @@ __device__ __forceinline__ FoldAcc fold_row_global(const float4* q, int n_grp, s
   return fold_seq(n_grp, [&](int p) { return __ldcg(q + p * stride); });
 }
 
-template <int MODE>
+template <int MODE, int S>
 __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params P) {
   extern __shared__ __align__(128) uint8_t tsm[];
   TailSmem& T = *reinterpret_cast<TailSmem*>(tsm);
@@ -776,14 +783,15 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   // Inputs are not written by K1 (the tables were produced before K1 passed its own wait), so
   // they are staged, and the masked-row list built, while K1 still streams.
   const int nb = max(0, min(*P.n_branches - P.branch_base, P.cap));
-  const int nt = nb * W;  // <= LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW = 2048
+  const int nt = nb * W;  // <= LOPA_MAX_ROWS
   const uint8_t* bmask = P.branch_mask + (size_t)P.branch_base * W;
   const int32_t* btok = P.branch_tokens + (size_t)P.branch_base * W;
-  uint32_t mine[4];  // thread owns rows 4 tid .. 4 tid + 3 (contiguous: ascending order)
+  constexpr int kRowsPerThread = LOPA_MAX_ROWS / kTailThreads;
+  uint32_t mine[kRowsPerThread];  // thread owns a contiguous run of rows (ascending order)
   int cnt = 0;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int idx = 4 * tid + u;
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    const int idx = kRowsPerThread * tid + u;
     const uint8_t mk = idx < nt ? bmask[idx] : (uint8_t)0;
     if (idx < nt) {
       T.msk[idx] = mk;
@@ -818,8 +826,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   {
     int pos = (int)s_wcnt[warp] + incl - cnt;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (mine[u]) rows[pos++] = (uint16_t)(4 * tid + u);
+    for (int u = 0; u < kRowsPerThread; ++u)
+      if (mine[u]) rows[pos++] = (uint16_t)(kRowsPerThread * tid + u);
   }
   const int n_masked = (int)s_wcnt[kTailThreads / 32];
   __syncthreads();
@@ -838,8 +846,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   }
   __syncthreads();
   if (tid == 0) { TL(7); TLC(19); }
-  if (MODE == MODE_STEP) cta_tail_step<kTailThreads>(P, T, tid);
-  if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads>(P, T, tid);
+  if (MODE == MODE_STEP) cta_tail_step<kTailThreads, S>(P, T, tid);
+  if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads, S>(P, T, tid);
   if (tid == 0) {
     P.ctrs[0] = 0;
     TL(5);
@@ -862,33 +870,35 @@ __global__ void __launch_bounds__(256) lopa_fold_kernel(const Params P) {
   if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrs[0] = 0;
 }
 
-static_assert(kTailThreads >= 4 * LOPA_MAX_WINDOW, "rank uses 4 threads per position");
-static_assert(4 * kTailThreads >= LOPA_MAX_BRANCHES * LOPA_MAX_WINDOW, "4 table rows per thread");
+static_assert(kTailThreads >= LOPA_MAX_WINDOW, "one tail thread per window position");
+static_assert(LOPA_MAX_ROWS % kTailThreads == 0, "rows per tail thread");
 
 constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + (2 * kStages + kItemSlots) * 8 +
                               kStages * 16 + kItemSlots * kPartPerItem * 16 + kItemSlots * 4 +
                               2 * kMaxGroups * 4 + 16;
 
 // ------------------------------------------------------------------ small decision kernels
+template <int S>
 __global__ void anchor_kernel(const float* conf, const int32_t* argmax, const int32_t* tokens,
-                              const uint8_t* mask, int W, float tau, int32_t* tok_out,
-                              uint8_t* msk_out, int32_t* dev_status) {
+                              const uint8_t* mask, int W, float tau, const float* tau_pos,
+                              int32_t* tok_out, uint8_t* msk_out, int32_t* dev_status) {
   const int lane = threadIdx.x;
-  WinRegs r;
-  load_window(r, conf, argmax, tokens, mask, W, lane);
-  const int st = warp_anchor(r, tau, lane);
+  WinRegs<S> r;
+  load_window<S>(r, conf, argmax, tokens, mask, W, lane);
+  const int st = warp_anchor<S>(r, tau, tau_pos, W, lane);
   if (st && lane == 0) atomicOr(dev_status, st);
-  store_window(r, tok_out, msk_out, W, lane);
+  store_window<S>(r, tok_out, msk_out, W, lane);
 }
 
+template <int S>
 __global__ void spawn_kernel(const float* conf, const int32_t* argmax, const int32_t* tok_b0,
                              const uint8_t* msk_b0, int W, int k, int32_t* br_tok,
                              uint8_t* br_msk, int32_t* look, int32_t* n_branches) {
-  __shared__ uint64_t keys[64];
+  __shared__ uint64_t keys[32 * S];
   const int lane = threadIdx.x;
-  WinRegs r;
-  load_window(r, conf, argmax, tok_b0, msk_b0, W, lane);
-  warp_spawn(r, W, k, keys, br_tok, br_msk, look, n_branches, lane);
+  WinRegs<S> r;
+  load_window<S>(r, conf, argmax, tok_b0, msk_b0, W, lane);
+  warp_spawn<S>(r, W, k, keys, br_tok, br_msk, look, n_branches, lane);
 }
 
 __global__ void verify_kernel(const float* conf, const uint8_t* mask, const int32_t* n_branches,
@@ -902,19 +912,20 @@ __global__ void verify_kernel(const float* conf, const uint8_t* mask, const int3
 }
 
 // Eq. 2 variants for the standalone call: one warp scores every branch in turn.
+template <int S>
 __global__ void verify_ex_kernel(const float* conf, const uint8_t* mask, const int32_t* n_branches,
                                  int max_br, int W, int metric, float param, float* scores,
                                  int32_t* winner) {
-  __shared__ double dscr[LOPA_MAX_WINDOW];
-  __shared__ float fscr[LOPA_MAX_WINDOW];
+  __shared__ double dscr[32 * S];
+  __shared__ float fscr[32 * S];
   const int lane = threadIdx.x;
   const int nb = max(0, min(*n_branches, max_br));
   float mine = -INFINITY;
   for (int j = 0; j < max_br; ++j) {
     float sc = -INFINITY;
     if (j < nb)
-      sc = warp_metric_score(conf + (size_t)j * W, mask + (size_t)j * W, W, metric, param, dscr,
-                             fscr, lane);
+      sc = warp_metric_score<S>(conf + (size_t)j * W, mask + (size_t)j * W, W, metric, param, dscr,
+                                fscr, lane);
     if (lane == 0) scores[j] = sc;
     if (lane == j) mine = sc;
   }
@@ -923,9 +934,10 @@ __global__ void verify_ex_kernel(const float* conf, const uint8_t* mask, const i
 }
 
 // Global half of a BP step: one warp; lane r reads record r's header.
+template <int S>
 __global__ void bp_finish_kernel(const Params P, const uint8_t* records, int world, int b_loc,
                                  int n_scores) {
-  __shared__ uint64_t keys[64];
+  __shared__ uint64_t keys[32 * S];
   const int lane = threadIdx.x;
   const size_t rb = record_bytes(b_loc);
   float bs = -INFINITY;
@@ -955,10 +967,10 @@ __global__ void bp_finish_kernel(const Params P, const uint8_t* records, int wor
   const int W = P.window;
   const bool none = (wid == 0xFFFFFFFFu) || (wid == 0x7FFFFFFFu);
   if (lane == 0) *P.winner = none ? 0 : (int)wid;
-  WinRegs r;
+  WinRegs<S> r;
   if (none) {  // no branch present anywhere: pass branch 0 through as complete
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < S; ++s) {
       const int i = lane + 32 * s;
       r.msk[s] = 0;
       r.tok[s] = i < W ? P.branch_tokens[i] : 0;
@@ -968,7 +980,7 @@ __global__ void bp_finish_kernel(const Params P, const uint8_t* records, int wor
   } else {
     RecordView rv = record_view(const_cast<uint8_t*>(records) + rb * owner, b_loc);
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < S; ++s) {
       const int i = lane + 32 * s;
       const bool in = i < W;
       r.msk[s] = in ? (uint32_t)(rv.mask[i] != 0) : 0u;
@@ -977,16 +989,19 @@ __global__ void bp_finish_kernel(const Params P, const uint8_t* records, int wor
       r.amax[s] = (in && r.msk[s]) ? rv.argmax[i] : -1;
     }
   }
-  const bool any = __ballot_sync(0xffffffffu, r.msk[0] | r.msk[1]) != 0;
+  bool anym = false;
+#pragma unroll
+  for (int s = 0; s < S; ++s) anym |= r.msk[s] != 0;
+  const bool any = __any_sync(0xffffffffu, anym);
   if (!any) {
-    store_window(r, P.next_tokens, P.next_mask, W, lane);
+    store_window<S>(r, P.next_tokens, P.next_mask, W, lane);
     if (P.lookahead)
       for (int q = lane; q < P.k; q += 32) P.lookahead[q] = -1;
     if (lane == 0) *P.n_next = 0;
     return;
   }
-  warp_anchor(r, P.tau, lane);
-  warp_spawn(r, W, P.k, keys, P.next_tokens, P.next_mask, P.lookahead, P.n_next, lane);
+  warp_anchor<S>(r, P.tau, P.tau_pos, W, lane);
+  warp_spawn<S>(r, W, P.k, keys, P.next_tokens, P.next_mask, P.lookahead, P.n_next, lane);
 }
 
 // ------------------------------------------------------------------ host helpers
@@ -1017,11 +1032,14 @@ static int ensure_kernel_attrs(int device) {
   if (major != 10 || minor != 0) return LOPA_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(lopa_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)kSmemBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(lopa_tail_kernel<MODE_STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kTailSmemBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(lopa_tail_kernel<MODE_BP_LOCAL>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kTailSmemBytes) != cudaSuccess)
+      cudaFuncSetAttribute(lopa_tail_kernel<MODE_STEP, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(lopa_tail_kernel<MODE_STEP, 8>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(lopa_tail_kernel<MODE_BP_LOCAL, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(lopa_tail_kernel<MODE_BP_LOCAL, 8>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess)
     return LOPA_ERR_CUDA;
   std::lock_guard<std::mutex> lk(g_mu);
   if (device >= 0 && device < 64) g_attr[device] = true;
@@ -1120,10 +1138,13 @@ static int launch_reduce(const Params& P, int device, cudaStream_t s) {
   if (P.mode == MODE_CONF) {
     const int nb = (P.n_cand + 255) / 256;
     e = launch_pdl(lopa_fold_kernel, dim3(nb), dim3(256), 0, s, P);
-  } else if (P.mode == MODE_STEP) {
-    e = launch_pdl(lopa_tail_kernel<MODE_STEP>, dim3(1), dim3(kTailThreads), kTailSmemBytes, s, P);
   } else {
-    e = launch_pdl(lopa_tail_kernel<MODE_BP_LOCAL>, dim3(1), dim3(kTailThreads), kTailSmemBytes, s, P);
+    // window slots per lane: 2 (W <= 64) or 8 (the D2F multi-block window, W <= 256)
+    const bool wide = P.window > 64;
+    auto kern = P.mode == MODE_STEP ? (wide ? lopa_tail_kernel<MODE_STEP, 8> : lopa_tail_kernel<MODE_STEP, 2>)
+                                    : (wide ? lopa_tail_kernel<MODE_BP_LOCAL, 8>
+                                            : lopa_tail_kernel<MODE_BP_LOCAL, 2>);
+    e = launch_pdl(kern, dim3(1), dim3(kTailThreads), kTailSmemBytes, s, P);
   }
   return cuda_status(e);
 }
@@ -1153,6 +1174,7 @@ int validate_step_args(const lopa_step_args_t* a, bool need_next) {
                     !a->n_branches_next || (a->k > 0 && !a->lookahead_pos)))
     return LOPA_ERR_INVALID_ARG;
   if (a->window > LOPA_MAX_WINDOW || a->vocab > LOPA_MAX_VOCAB) return LOPA_ERR_UNSUPPORTED;
+  if (a->window > 64 && a->vocab > (1 << 22)) return LOPA_ERR_UNSUPPORTED;  // R24 exact sums
   if (a->max_branches > LOPA_MAX_BRANCHES || a->k + 1 > LOPA_MAX_BRANCHES)
     return LOPA_ERR_UNSUPPORTED;
   return LOPA_OK;
@@ -1177,6 +1199,7 @@ static Params base_params(const lopa_step_args_t* a, const Workspace& ws) {
   P.branch_mask = a->branch_mask;
   P.k = a->k;
   P.tau = a->tau;
+  P.tau_pos = a->tau_pos;
   P.metric = a->metric;
   P.metric_param = a->metric_param;
   P.scores = a->scores;
@@ -1223,8 +1246,12 @@ int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, co
   Workspace ws{};
   Params P = base_params(a, ws);
   const int n_scores = a->max_branches;
-  bp_finish_kernel<<<1, 32, 0, s>>>(P, static_cast<const uint8_t*>(records), world, b_loc,
-                                    n_scores);
+  if (a->window > 64)
+    bp_finish_kernel<8><<<1, 32, 0, s>>>(P, static_cast<const uint8_t*>(records), world, b_loc,
+                                         n_scores);
+  else
+    bp_finish_kernel<2><<<1, 32, 0, s>>>(P, static_cast<const uint8_t*>(records), world, b_loc,
+                                         n_scores);
   return cuda_status(cudaGetLastError());
 }
 
@@ -1343,20 +1370,32 @@ extern "C" int lopa_confidence(const void* logits, int64_t ld, int32_t n_rows, i
   return launch_reduce(P, dev, s);
 }
 
-extern "C" int lopa_anchor_fill(const float* conf, const int32_t* argmax, const int32_t* tokens,
-                                const uint8_t* mask, int32_t window, float tau,
-                                int32_t* tokens_out, uint8_t* mask_out, int32_t* dev_status,
-                                void* stream) {
+extern "C" int lopa_anchor_fill_ex(const float* conf, const int32_t* argmax, const int32_t* tokens,
+                                   const uint8_t* mask, int32_t window, float tau,
+                                   const float* tau_pos, int32_t* tokens_out, uint8_t* mask_out,
+                                   int32_t* dev_status, void* stream) {
   if (!conf || !argmax || !tokens || !mask || !tokens_out || !mask_out || !dev_status)
     return LOPA_ERR_INVALID_ARG;
   if (window < 1 || !(tau > 0.f && tau <= 1.f)) return LOPA_ERR_INVALID_ARG;
   if (window > LOPA_MAX_WINDOW) return LOPA_ERR_UNSUPPORTED;
   int dev;
   if (!bind_device(stream, conf, &dev)) return LOPA_ERR_CUDA;
-  anchor_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(conf, argmax, tokens, mask, window,
-                                                                  tau, tokens_out, mask_out,
-                                                                  dev_status);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (window > 64)
+    anchor_kernel<8><<<1, 32, 0, s>>>(conf, argmax, tokens, mask, window, tau, tau_pos, tokens_out,
+                                      mask_out, dev_status);
+  else
+    anchor_kernel<2><<<1, 32, 0, s>>>(conf, argmax, tokens, mask, window, tau, tau_pos, tokens_out,
+                                      mask_out, dev_status);
   return cuda_status(cudaGetLastError());
+}
+
+extern "C" int lopa_anchor_fill(const float* conf, const int32_t* argmax, const int32_t* tokens,
+                                const uint8_t* mask, int32_t window, float tau,
+                                int32_t* tokens_out, uint8_t* mask_out, int32_t* dev_status,
+                                void* stream) {
+  return lopa_anchor_fill_ex(conf, argmax, tokens, mask, window, tau, nullptr, tokens_out,
+                             mask_out, dev_status, stream);
 }
 
 extern "C" int lopa_spawn_branches(const float* conf, const int32_t* argmax,
@@ -1371,9 +1410,14 @@ extern "C" int lopa_spawn_branches(const float* conf, const int32_t* argmax,
   if (window > LOPA_MAX_WINDOW || k + 1 > LOPA_MAX_BRANCHES) return LOPA_ERR_UNSUPPORTED;
   int dev;
   if (!bind_device(stream, conf, &dev)) return LOPA_ERR_CUDA;
-  spawn_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
-      conf, argmax, tokens_b0, mask_b0, window, k, branch_tokens, branch_mask, lookahead_pos,
-      n_branches);
+  if (window > 64)
+    spawn_kernel<8><<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        conf, argmax, tokens_b0, mask_b0, window, k, branch_tokens, branch_mask, lookahead_pos,
+        n_branches);
+  else
+    spawn_kernel<2><<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        conf, argmax, tokens_b0, mask_b0, window, k, branch_tokens, branch_mask, lookahead_pos,
+        n_branches);
   return cuda_status(cudaGetLastError());
 }
 
@@ -1401,8 +1445,12 @@ extern "C" int lopa_verify_select_ex(const float* conf, const uint8_t* branch_ma
   if (window > LOPA_MAX_WINDOW || max_branches > LOPA_MAX_BRANCHES) return LOPA_ERR_UNSUPPORTED;
   int dev;
   if (!bind_device(stream, conf, &dev)) return LOPA_ERR_CUDA;
-  verify_ex_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
-      conf, branch_mask, n_branches, max_branches, window, metric, metric_param, scores, winner);
+  if (window > 64)
+    verify_ex_kernel<8><<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        conf, branch_mask, n_branches, max_branches, window, metric, metric_param, scores, winner);
+  else
+    verify_ex_kernel<2><<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        conf, branch_mask, n_branches, max_branches, window, metric, metric_param, scores, winner);
   return cuda_status(cudaGetLastError());
 }
 

@@ -1,8 +1,10 @@
-// Warp-level LoPA decisions (one warp owns a window of W <= 64 positions and <= 32 branches):
-//   Eq. 2 branch scores + select, Eq. 1 anchor,
-//   top-k lookahead spawn.
-// Lane l owns positions l and l + 32.  All decisions are exact functions of the fp32 conf
-// bits: ordered integer keys, ballots and rank counting — no floating-point reassociation.
+// Warp-level LoPA decisions over a window of W <= 32*S positions (S = 2 for W <= 64, S = 8 for
+// the D2F multi-block window up to 256) and <= 32 branches:
+//   Eq. 2 branch scores (+ the P:204 variants) and select, Eq. 1 anchor
+//    with a per-position threshold (D2F), top-k lookahead spawn
+//   (P:167-171).
+// Lane l owns positions l + 32 h, h < S.  All decisions are exact functions of the fp32 conf bits:
+// ordered integer keys, ballots and rank counting — no floating-point reassociation.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -14,13 +16,13 @@ namespace lopa {
 constexpr int kDevEmptyMask = 1;
 constexpr int kDevNonfinite = 2;
 
-// Position state of one window held in registers: lane owns slots 0 (i = lane) and 1
-// (i = lane + 32).
+// Position state of one window held in registers.
+template <int S>
 struct WinRegs {
-  float conf[2];
-  int32_t amax[2];
-  int32_t tok[2];
-  uint32_t msk[2];  // 1 = masked
+  float conf[S];
+  int32_t amax[S];
+  int32_t tok[S];
+  uint32_t msk[S];  // 1 = masked
 };
 
 // Order-preserving map of a float to uint32 (for non-NaN values; -inf is smallest).
@@ -30,12 +32,13 @@ __device__ __forceinline__ uint32_t ordered_bits(float f) {
 }
 
 // Load the window row of branch state (tok/msk) and conf/argmax.  conf / msk may point to shared
-// memory (generic loads); amax is global and read L2-coherently (written by other CTAs).
-__device__ __forceinline__ void load_window(WinRegs& r, const float* conf, const int32_t* amax,
+// memory (generic loads); amax is read L2-coherently.
+template <int S>
+__device__ __forceinline__ void load_window(WinRegs<S>& r, const float* conf, const int32_t* amax,
                                             const int32_t* tok, const uint8_t* msk, int W,
                                             int lane) {
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < S; ++s) {
     const int i = lane + 32 * s;
     const bool in = i < W;
     r.msk[s] = in ? (uint32_t)(msk[i] != 0) : 0u;
@@ -45,10 +48,8 @@ __device__ __forceinline__ void load_window(WinRegs& r, const float* conf, const
   }
 }
 
-// Eq. 2: lane j < n_br scores branch j: sum of conf over its masked positions in
-// position order (fp64), divided by the count, rounded once to fp32; 1.0 if none (R8).
-// Absent branches (n_br <= j < max_br) score -inf.  Returns the branch's score in lane j.
-// conf / mask are generic pointers (shared memory in the fused tail).
+// Eq. 2: lane j < n_br scores branch j (mean of conf over its masked positions, fp64,
+// rounded once to fp32; 1.0 if none, R8).  Absent branches score -inf.
 __device__ __forceinline__ float warp_branch_score(const float* conf, const uint8_t* mask,
                                                    int n_br, int max_br, int W, int lane) {
   float score = -INFINITY;
@@ -74,55 +75,71 @@ constexpr int kMetricMean = 0;            // Eq. 2: mean over M_Bj
 constexpr int kMetricSlidingMin = 1;      // min over length-w windows (position order) of the mean
 constexpr int kMetricBottomFraction = 2;  // mean of the ceil(eta * |M_Bj|) lowest confidences
 
-// C(B_j) of one branch with a full warp (lane owns positions lane and lane + 32).  conf / mask are
-// generic pointers; dscr (64 doubles) and fscr (64 floats) are per-warp shared scratch.  Every sum
-// is an exact fp64 sum (each conf lies in [2^-23, 1], at most 64 terms), so the value equals the
-// oracle's fp64 value whatever the summation order, rounded once to fp32.  1.0 if M_Bj is empty.
+// C(B_j) of one branch with a full warp.  conf / mask are generic pointers; dscr (32 S doubles) and
+// fscr (32 S floats) are per-warp shared scratch.  Every sum is an exact fp64 sum (reading R24:
+// each conf is an fp32 value >= 1/V, so its lowest significant bit is >= 2^-(23 + ceil(log2 V));
+// with <= W terms the sum stays below 2^ceil(log2 W); the host enforces
+// ceil(log2 W) + 23 + ceil(log2 V) <= 53), so the value equals the oracle's fp64 value whatever
+// the order, rounded once to fp32.  1.0 if M_Bj is empty.
+template <int S>
 __device__ __forceinline__ float warp_metric_score(const float* conf, const uint8_t* mask, int W,
                                                    int metric, float param, double* dscr,
                                                    float* fscr, int lane) {
-  bool m[2];
-  double v[2];
+  bool m[S];
+  double v[S];
+  uint32_t b[S];
+  int n = 0;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < S; ++h) {
     const int i = lane + 32 * h;
     m[h] = i < W && mask[i] != 0;
     v[h] = m[h] ? (double)conf[i] : 0.0;
+    b[h] = __ballot_sync(0xffffffffu, m[h]);
+    n += __popc(b[h]);
   }
-  const uint32_t b0 = __ballot_sync(0xffffffffu, m[0]), b1 = __ballot_sync(0xffffffffu, m[1]);
-  const int n = __popc(b0) + __popc(b1);
   if (n == 0) return 1.0f;
   if (metric == kMetricMean) {
-    double s = v[0] + v[1];
+    double s = 0.0;
+#pragma unroll
+    for (int h = 0; h < S; ++h) s += v[h];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     return (float)(s / (double)n);
   }
   const uint32_t lt = (1u << lane) - 1u;
-  const int idx[2] = {__popc(b0 & lt), __popc(b0) + __popc(b1 & lt)};
+  int idx[S];
+  {
+    int base = 0;
+#pragma unroll
+    for (int h = 0; h < S; ++h) {
+      idx[h] = base + __popc(b[h] & lt);
+      base += __popc(b[h]);
+    }
+  }
   float result;
   if (metric == kMetricSlidingMin) {
     const int w = min(max((int)param, 1), n);
     // inclusive prefix sums in position (= compacted) order, stored by compacted index
-    double P[2];
+    double P[S];
+    double carry = 0.0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < S; ++h) {
       double x = v[h];
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         const double y = __shfl_up_sync(0xffffffffu, x, off);
         if (lane >= off) x += y;
       }
-      P[h] = x;
+      P[h] = x + carry;
+      carry += __shfl_sync(0xffffffffu, x, 31);
     }
-    P[1] += __shfl_sync(0xffffffffu, P[0], 31);
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < S; ++h)
       if (m[h]) dscr[idx[h]] = P[h];
     __syncwarp();
     double best = INFINITY;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < S; ++h) {
       if (m[h] && idx[h] >= w - 1) {
         const double lo = idx[h] - w >= 0 ? dscr[idx[h] - w] : 0.0;
         best = fmin(best, (P[h] - lo) / (double)w);
@@ -132,31 +149,30 @@ __device__ __forceinline__ float warp_metric_score(const float* conf, const uint
     for (int off = 16; off > 0; off >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, off));
     result = (float)best;
   } else {  // kMetricBottomFraction
-    const int b = (int)ceil((double)param * (double)n);
+    const int bcnt = (int)ceil((double)param * (double)n);
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < S; ++h)
       if (m[h]) fscr[idx[h]] = (float)v[h];
     __syncwarp();
     double s = 0.0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < S; ++h) {
       if (m[h]) {
         const float x = (float)v[h];
         int r = 0;
         for (int q = 0; q < n; ++q) r += (fscr[q] < x || (fscr[q] == x && q < idx[h])) ? 1 : 0;
-        if (r < b) s += v[h];
+        if (r < bcnt) s += v[h];
       }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    result = (float)(s / (double)b);
+    result = (float)(s / (double)bcnt);
   }
   __syncwarp();
   return result;
 }
 
-// Select (R9): smallest j with the largest fp32 score.  Scores are never NaN-free
-// guaranteed (a NONFINITE row poisons its branch); NaN scores lose (treated as -inf).
+// Select (R9): smallest j with the largest fp32 score (NaN scores lose).
 __device__ __forceinline__ int warp_select(float score, int lane, int n_lanes_valid) {
   const float s = (lane < n_lanes_valid && !isnan(score)) ? score : -INFINITY;
   const uint32_t key = ordered_bits(s);
@@ -167,17 +183,25 @@ __device__ __forceinline__ int warp_select(float score, int lane, int n_lanes_va
 }
 
 // Eq. 1 + Alg. 1 step 1 on the window in registers: fills I_fill in place (r becomes B0).
+// tau_pos (nullable): per-position thresholds (D2F window: tau_act / tau_conf per block).
 // Returns LOPA_DEV_EMPTY_MASK if nothing is masked (state unchanged), else 0.
-__device__ __forceinline__ int warp_anchor(WinRegs& r, float tau, int lane) {
-  bool high[2];
+template <int S>
+__device__ __forceinline__ int warp_anchor(WinRegs<S>& r, float tau, const float* tau_pos, int W,
+                                           int lane) {
+  bool high[S];
+  bool anym = false, anyh = false;
 #pragma unroll
-  for (int s = 0; s < 2; ++s) high[s] = r.msk[s] && (r.conf[s] > tau);
-  const uint32_t any_masked = __ballot_sync(0xffffffffu, r.msk[0] | r.msk[1]);
-  if (!any_masked) return kDevEmptyMask;
-  const uint32_t any_high = __ballot_sync(0xffffffffu, high[0] | high[1]);
-  if (any_high) {
+  for (int s = 0; s < S; ++s) {
+    const int i = lane + 32 * s;
+    const float t = (tau_pos && i < W) ? tau_pos[i] : tau;
+    high[s] = r.msk[s] && (r.conf[s] > t);
+    anym |= r.msk[s] != 0;
+    anyh |= high[s];
+  }
+  if (!__any_sync(0xffffffffu, anym)) return kDevEmptyMask;
+  if (__any_sync(0xffffffffu, anyh)) {
 #pragma unroll
-    for (int s = 0; s < 2; ++s)
+    for (int s = 0; s < S; ++s)
       if (high[s]) {
         r.tok[s] = r.amax[s];
         r.msk[s] = 0;
@@ -185,15 +209,17 @@ __device__ __forceinline__ int warp_anchor(WinRegs& r, float tau, int lane) {
     return 0;
   }
   // Fallback (Eq. 1 "otherwise"): argmax conf over M_t, lowest position on ties (R5).
-  uint32_t k0 = r.msk[0] ? ordered_bits(r.conf[0]) : 0u;
-  uint32_t k1 = r.msk[1] ? ordered_bits(r.conf[1]) : 0u;
-  const uint32_t best = __reduce_max_sync(0xffffffffu, max(k0, k1));
+  uint32_t kmax = 0u;
+#pragma unroll
+  for (int s = 0; s < S; ++s) kmax = max(kmax, r.msk[s] ? ordered_bits(r.conf[s]) : 0u);
+  const uint32_t best = __reduce_max_sync(0xffffffffu, kmax);
   uint32_t cand = 0xffffffffu;
-  if (r.msk[1] && k1 == best) cand = (uint32_t)(lane + 32);
-  if (r.msk[0] && k0 == best) cand = (uint32_t)lane;
+#pragma unroll
+  for (int s = S - 1; s >= 0; --s)
+    if (r.msk[s] && ordered_bits(r.conf[s]) == best) cand = (uint32_t)(lane + 32 * s);
   const uint32_t istar = __reduce_min_sync(0xffffffffu, cand);
 #pragma unroll
-  for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < S; ++s)
     if ((uint32_t)(lane + 32 * s) == istar) {
       r.tok[s] = r.amax[s];
       r.msk[s] = 0;
@@ -201,39 +227,36 @@ __device__ __forceinline__ int warp_anchor(WinRegs& r, float tau, int lane) {
   return 0;
 }
 
-// Alg. 1 step 2: rank of every position of M_B0 under (conf desc, position asc)
-// by counting, n = min(k, |M_B0|).  `keys` is a 64-entry per-warp shared scratch.
+// Alg. 1 step 2 with one warp: rank of every position of M_B0 under (conf desc,
+// position asc) by counting, n = min(k, |M_B0|).  `keys` is 32 S entries of shared scratch.
 // Writes branch tables rows 0..n, lookahead_pos[0..k), *n_branches = n + 1.
-__device__ __forceinline__ void warp_spawn(const WinRegs& b0, int W, int k, uint64_t* keys,
+template <int S>
+__device__ __forceinline__ void warp_spawn(const WinRegs<S>& b0, int W, int k, uint64_t* keys,
                                            int32_t* br_tok, uint8_t* br_msk, int32_t* look,
                                            int32_t* n_branches, int lane) {
-  // key = ordered conf bits << 32 | (63 - i): larger key = earlier in the order.
+  // key = ordered conf bits << 32 | (32 S - 1 - i): larger key = earlier in the order.
+  int n_mb0 = 0;
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < S; ++s) {
     const int i = lane + 32 * s;
-    keys[i] = b0.msk[s] ? (((uint64_t)ordered_bits(b0.conf[s]) << 32) | (uint64_t)(63 - i))
+    keys[i] = b0.msk[s] ? (((uint64_t)ordered_bits(b0.conf[s]) << 32) | (uint64_t)(32 * S - 1 - i))
                         : 0ull;
+    n_mb0 += __popc(__ballot_sync(0xffffffffu, b0.msk[s]));
   }
   __syncwarp();
-  const int n_mb0 = __popc(__ballot_sync(0xffffffffu, b0.msk[0])) +
-                    __popc(__ballot_sync(0xffffffffu, b0.msk[1]));
   const int n = min(k, n_mb0);
-  int rank[2];
+  int rank[S];
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < S; ++s) {
     const uint64_t mine = keys[lane + 32 * s];
     int cnt = 0;
 #pragma unroll 8
-    for (int q = 0; q < 64; ++q) cnt += (keys[q] > mine) ? 1 : 0;
+    for (int q = 0; q < 32 * S; ++q) cnt += (keys[q] > mine) ? 1 : 0;
     rank[s] = b0.msk[s] ? cnt : 1 << 20;
   }
   __syncwarp();
-#ifdef TL
-  if (lane == 0) TL(12);
-#endif
-  // Branch j (1..n) fills p_j = the position of rank j - 1.
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < S; ++s) {
     const int i = lane + 32 * s;
     if (rank[s] < n && look) look[rank[s]] = i;
   }
@@ -241,7 +264,7 @@ __device__ __forceinline__ void warp_spawn(const WinRegs& b0, int W, int k, uint
     for (int q = n + lane; q < k; q += 32) look[q] = -1;
   for (int j = 0; j <= n; ++j) {
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < S; ++s) {
       const int i = lane + 32 * s;
       if (i < W) {
         const bool fill = (j >= 1) && (rank[s] == j - 1);
@@ -251,16 +274,14 @@ __device__ __forceinline__ void warp_spawn(const WinRegs& b0, int W, int k, uint
     }
   }
   if (lane == 0) *n_branches = n + 1;
-#ifdef TL
-  if (lane == 0) TL(13);
-#endif
 }
 
 // Store the window registers to a table row.
-__device__ __forceinline__ void store_window(const WinRegs& r, int32_t* tok, uint8_t* msk, int W,
+template <int S>
+__device__ __forceinline__ void store_window(const WinRegs<S>& r, int32_t* tok, uint8_t* msk, int W,
                                              int lane) {
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < S; ++s) {
     const int i = lane + 32 * s;
     if (i < W) {
       tok[i] = r.tok[s];

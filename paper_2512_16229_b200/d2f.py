@@ -1,0 +1,181 @@
+"""D2F block pipeline around the fused LoPA step.
+
+"LoPA integrates seamlessly with D2F by treating all active blocks as a single window for
+branch exploration".  The window is the union of the active blocks (contiguous:
+blocks activate and commit in index order), up to LOPA_MAX_WINDOW = 256 positions; every
+iteration is ONE `lopa_step` launch over that window with per-position Eq. 1 thresholds
+(tau_act on the newest active block, tau_conf on older ones — reading R25).  The block rules
+are reading R26 (D2F's parameters from the Appendix table,
+PAPER.md:519-536):
+
+  (a) after each step, active blocks that the selected branch B* fills completely are
+      committed, oldest first, stopping at the first block that is not full;
+  (b) if no block is active the next one is activated; otherwise the next block is activated
+      when the newest active block's fill ratio >= tau_add and the window stays <= max_window;
+  the spawned branches carry over: committed columns are dropped, newly activated columns are
+  appended fully masked; a step that completes its window (R21) is followed by the new
+  window's initial predict (R17).
+
+This module is host control flow only (a few integers per iteration); all per-position work
+is in liblopa's kernels.  It never imports the oracle.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import lopa
+
+INACTIVE, ACTIVE, COMMITTED = 0, 1, 2
+
+
+@dataclass
+class BlockConfig:
+    """D2F parameters (Appendix table)."""
+    block_size: int = 32
+    tau_add: float = 0.1
+    tau_act: float = 0.95
+    tau_conf: float = 0.90
+    max_window: int = lopa.MAX_WINDOW
+
+
+@dataclass
+class D2FResult:
+    tokens: torch.Tensor                      # int32 [gen_len] on the device
+    forwards: int = 0
+    windows: list = field(default_factory=list)
+    winners: list = field(default_factory=list)
+    branch_counts: list = field(default_factory=list)
+    commits: list = field(default_factory=list)
+
+    @property
+    def tpf(self) -> float:
+        return self.tokens.numel() / self.forwards if self.forwards else 0.0
+
+
+class BlockPipeline:
+    """Block status bookkeeping (R26).  Status per block: INACTIVE -> ACTIVE -> COMMITTED."""
+
+    def __init__(self, n_blocks: int, cfg: BlockConfig):
+        if cfg.block_size < 1 or cfg.block_size > cfg.max_window or cfg.max_window > lopa.MAX_WINDOW:
+            raise lopa.LopaError("block_size must be in [1, max_window] and max_window <= 256")
+        self.cfg = cfg
+        self.status = [INACTIVE] * n_blocks
+        self.status[0] = ACTIVE
+
+    def active(self):
+        return [b for b, s in enumerate(self.status) if s == ACTIVE]
+
+    def window(self):
+        """(first position, width) of the active window."""
+        a = self.active()
+        B = self.cfg.block_size
+        return (a[0] * B, len(a) * B) if a else (0, 0)
+
+    def thresholds(self):
+        """Per-position Eq. 1 thresholds over the window (float32 list)."""
+        a = self.active()
+        B = self.cfg.block_size
+        out = []
+        for b in a:
+            out += [self.cfg.tau_act if b == a[-1] else self.cfg.tau_conf] * B
+        return out
+
+    def update(self, masked_per_block):
+        """Apply rules (a), (b).  masked_per_block[b] = masked count of B* in block b (active
+        blocks only).  Returns the list of newly committed blocks."""
+        st, B = self.status, self.cfg.block_size
+        committed = []
+        for b in range(len(st)):
+            if st[b] == COMMITTED:
+                continue
+            if st[b] == ACTIVE and masked_per_block[b] == 0:
+                st[b] = COMMITTED
+                committed.append(b)
+                continue
+            break
+        a = self.active()
+        nxt = next((b for b, s in enumerate(st) if s == INACTIVE), None)
+        if nxt is not None:
+            if not a:
+                st[nxt] = ACTIVE
+            elif ((B - masked_per_block[a[-1]]) / B >= float(self.cfg.tau_add)
+                  and (len(a) + 1) * B <= self.cfg.max_window):
+                st[nxt] = ACTIVE
+        return committed
+
+    def done(self):
+        return all(s == COMMITTED for s in self.status)
+
+
+def decode_d2f(forward_block, gen_len: int, k: int, cfg: BlockConfig, vocab: int, device,
+               tokens0: torch.Tensor | None = None, max_forwards: int | None = None,
+               metric: int = lopa.METRIC_MEAN, metric_param: float = 0.0) -> D2FResult:
+    """LoPA decoding of a ``gen_len``-token region through the D2F block pipeline.
+
+    ``forward_block(b, tokens[n][B], mask[n][B]) -> bf16 [n][B][ld]`` is the model stand-in for
+    the positions of block b under n branch states (device tensors); a window forward is one
+    call per active block, placed side by side in the window's logits buffer."""
+    B = cfg.block_size
+    if gen_len % B:
+        raise lopa.LopaError("gen_len must be a multiple of block_size")
+    dev = torch.device(device)
+    n_blk = gen_len // B
+    pipe = BlockPipeline(n_blk, cfg)
+    tok = torch.zeros(gen_len, dtype=torch.int32, device=dev) if tokens0 is None else tokens0.clone()
+    msk = torch.ones(gen_len, dtype=torch.uint8, device=dev)
+    max_br = k + 1
+    ld = ((vocab + 7) // 8) * 8
+    steppers = {}
+    res = D2FResult(tokens=tok)
+    p0, W = pipe.window()
+    br_tok = torch.zeros((max_br, W), dtype=torch.int32, device=dev)
+    br_msk = torch.zeros((max_br, W), dtype=torch.uint8, device=dev)
+    br_tok[0], br_msk[0] = tok[p0:p0 + W], msk[p0:p0 + W]
+    n = 1
+    nb_dev = torch.ones(1, dtype=torch.int32, device=dev)
+    while True:
+        if W not in steppers:
+            tp = torch.empty(W, dtype=torch.float32, device=dev)
+            steppers[W] = (lopa.Stepper(vocab, W, max_br, k, cfg.tau_act, dev, metric=metric,
+                                        metric_param=metric_param, tau_pos=tp),
+                           torch.empty((max_br, W, ld), dtype=torch.bfloat16, device=dev))
+        st, logits = steppers[W]
+        st.tau_pos.copy_(torch.tensor(pipe.thresholds(), dtype=torch.float32))
+        for c, b in enumerate(pipe.active()):
+            logits[:n, c * B:(c + 1) * B] = forward_block(b, br_tok[:n, c * B:(c + 1) * B].contiguous(),
+                                                           br_msk[:n, c * B:(c + 1) * B].contiguous())
+        nb_dev.fill_(n)
+        out = st.step(logits, nb_dev, br_tok, br_msk)
+        res.forwards += 1
+        res.windows.append((p0, W))
+        res.branch_counts.append(n)
+        w, n_next = (int(x) for x in torch.stack([out.winner[0], out.n_next[0]]).cpu())
+        res.winners.append(w)
+        # x_{t+1} = B* on the window
+        tok[p0:p0 + W] = br_tok[w]
+        msk[p0:p0 + W] = br_msk[w]
+        masked = msk.view(n_blk, B).sum(dim=1).cpu().tolist()
+        res.commits += pipe.update(masked)
+        if pipe.done() or (max_forwards is not None and res.forwards >= max_forwards):
+            break
+        q0, WN = pipe.window()
+        nt = torch.zeros((max_br, WN), dtype=torch.int32, device=dev)
+        nm = torch.zeros((max_br, WN), dtype=torch.uint8, device=dev)
+        if n_next == 0:
+            # the window is complete (R21): the new window starts with its initial predict
+            nt[0], nm[0] = tok[q0:q0 + WN], msk[q0:q0 + WN]
+            n = 1
+        else:
+            # carry the spawned branches over: keep the surviving columns, append new blocks
+            lo, hi = max(p0, q0), min(p0 + W, q0 + WN)
+            nt[:n_next] = tok[q0:q0 + WN]
+            nm[:n_next] = msk[q0:q0 + WN]
+            if hi > lo:
+                nt[:n_next, lo - q0:hi - q0] = out.next_tokens[:n_next, lo - p0:hi - p0]
+                nm[:n_next, lo - q0:hi - q0] = out.next_mask[:n_next, lo - p0:hi - p0]
+            n = n_next
+        p0, W, br_tok, br_msk = q0, WN, nt, nm
+    res.tokens = tok
+    return res

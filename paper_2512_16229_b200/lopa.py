@@ -26,7 +26,7 @@ METRIC_SLIDING_MIN = 1     # P:204 sliding window
 METRIC_BOTTOM_FRACTION = 2 # P:204 least-confident segment
 DEV_EMPTY_MASK = 1
 DEV_NONFINITE = 2
-MAX_WINDOW = 64
+MAX_WINDOW = 256
 MAX_BRANCHES = 32
 MAX_ROWS = 4096
 UNIQUE_ID_BYTES = 128
@@ -53,7 +53,7 @@ class StepArgs(ctypes.Structure):
         ("next_tokens", _c_void_p), ("next_mask", _c_void_p), ("lookahead_pos", _c_void_p),
         ("n_branches_next", _c_void_p), ("dev_status", _c_void_p),
         ("workspace", _c_void_p), ("workspace_bytes", _size),
-        ("metric", _i32), ("metric_param", _f32),
+        ("metric", _i32), ("metric_param", _f32), ("tau_pos", _c_void_p),
     ]
 
 
@@ -66,6 +66,8 @@ _SIGS = {
                                _c_void_p, _c_void_p, _size, _c_void_p]),
     "lopa_anchor_fill": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _f32,
                                 _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
+    "lopa_anchor_fill_ex": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _f32, _c_void_p,
+                                   _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_spawn_branches": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _i32,
                                    _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_verify_select": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i32, _i32, _c_void_p,
@@ -175,18 +177,20 @@ def confidence(logits: torch.Tensor, vocab: int | None = None, row_mask: torch.T
 
 
 # ----------------------------------------------------------------------------- a3
-def anchor_fill(conf, argmax, tokens, mask, tau: float, status=None):
-    """Eq. 1 + Alg. 1 step 1.  Returns (tokens_B0, mask_B0, status)."""
-    _need_cuda(conf, argmax, tokens, mask)
+def anchor_fill(conf, argmax, tokens, mask, tau: float, status=None, tau_pos=None):
+    """Eq. 1 + Alg. 1 step 1.  tau_pos: optional per-position thresholds
+    (float32 [W], the D2F window).  Returns (tokens_B0, mask_B0, status)."""
+    _need_cuda(conf, argmax, tokens, mask, tau_pos)
     W = mask.numel()
     dev = mask.device
     tok_out = torch.empty(W, dtype=torch.int32, device=dev)
     msk_out = torch.empty(W, dtype=torch.uint8, device=dev)
     status = new_status(dev) if status is None else status
-    _check(lib().lopa_anchor_fill(_p(conf.contiguous()), _p(argmax.contiguous()),
-                                  _p(tokens.contiguous()), _p(_u8(mask).contiguous()), W, tau,
-                                  _p(tok_out), _p(msk_out), _p(status), _stream(dev)),
-           "lopa_anchor_fill")
+    tp = None if tau_pos is None else tau_pos.contiguous()
+    _check(lib().lopa_anchor_fill_ex(_p(conf.contiguous()), _p(argmax.contiguous()),
+                                     _p(tokens.contiguous()), _p(_u8(mask).contiguous()), W, tau,
+                                     _p(tp), _p(tok_out), _p(msk_out), _p(status), _stream(dev)),
+           "lopa_anchor_fill_ex")
     return tok_out, msk_out, status
 
 
@@ -249,9 +253,11 @@ class Stepper:
     configuration, so that repeated steps allocate nothing (CUDA-graph friendly)."""
 
     def __init__(self, vocab: int, window: int, max_branches: int, k: int, tau: float, device,
-                 ld: int | None = None, metric: int = METRIC_MEAN, metric_param: float = 0.0):
+                 ld: int | None = None, metric: int = METRIC_MEAN, metric_param: float = 0.0,
+                 tau_pos: torch.Tensor | None = None):
         self.vocab, self.window, self.max_branches, self.k, self.tau = vocab, window, max_branches, k, tau
         self.metric, self.metric_param = metric, metric_param
+        self.tau_pos = tau_pos  # optional device float32 [window] (D2F per-position thresholds)
         self.ld = ld if ld is not None else ((vocab + 7) // 8) * 8
         self.device = torch.device(device)
         d = self.device
@@ -279,7 +285,8 @@ class Stepper:
             next_tokens=o.next_tokens.data_ptr(), next_mask=o.next_mask.data_ptr(),
             lookahead_pos=o.lookahead.data_ptr(), n_branches_next=o.n_next.data_ptr(),
             dev_status=o.status.data_ptr(), workspace=self.ws.data_ptr(),
-            workspace_bytes=self.ws.numel(), metric=self.metric, metric_param=self.metric_param)
+            workspace_bytes=self.ws.numel(), metric=self.metric, metric_param=self.metric_param,
+            tau_pos=None if self.tau_pos is None else self.tau_pos.data_ptr())
 
     def _validate(self, logits, n_branches, branch_tokens, branch_mask):
         _need_cuda(logits, n_branches, branch_tokens, branch_mask)

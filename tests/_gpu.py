@@ -38,8 +38,8 @@ def decision_gaps(conf_w, mask_w, anchor_mask, k, tau, scores):
     gaps["select"] = (s[0] - s[1]) if len(s) > 1 else np.inf
     M = [i for i in range(len(mask_w)) if mask_w[i]]
     if M:
-        t = O.tau_as_f64(tau)
-        gaps["anchor"] = min(abs(float(conf_w[i]) - t) for i in M)
+        t = np.broadcast_to(np.asarray(tau, np.float32).astype(np.float64), (len(mask_w),))
+        gaps["anchor"] = min(abs(float(conf_w[i]) - t[i]) for i in M)
         c = sorted((float(conf_w[i]) for i in M), reverse=True)
         gaps["fallback"] = (c[0] - c[1]) if len(c) > 1 else np.inf
     if anchor_mask is not None:

@@ -1,0 +1,54 @@
+"""GPU parity of the D2F block pipeline (paper_2512_16229_b200/d2f.py, NEXT-1, R25,
+R26): the product loop — one fused `lopa_step` per iteration over the multi-block window with
+per-position thresholds — against the oracle loop (oracle/d2f_oracle.py) on the same SYN-D2F
+forward.  Whole traces must agree: windows, branch counts, winners, commit order, final
+tokens and forward counts."""
+import numpy as np
+import pytest
+import torch
+
+import syngen
+from oracle import d2f_oracle as D
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def mods():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2512_16229_b200 import d2f, lopa
+    return d2f, lopa
+
+
+def _compare(mods, seed, V, L, B, k, tau_add, tau_act, tau_conf, max_window, extras):
+    d2f, lopa = mods
+    cfg = d2f.BlockConfig(B, tau_add, tau_act, tau_conf, max_window)
+    g = d2f.decode_d2f(lambda b, t, m: lopa.syn_generate(seed, b, V, t, m, extras=extras),
+                       L, k, cfg, V, DEV)
+    r = D.decode_d2f(lambda b, t, m: syngen.gen_logits(seed, b, V, t, m, extras=extras),
+                     L, B, k, tau_add, tau_act, tau_conf, max_window=max_window)
+    assert g.windows == r.windows
+    assert g.branch_counts == r.branch_counts
+    assert g.winners == r.winners
+    assert g.commits == r.commits
+    assert g.forwards == r.forwards
+    assert np.array_equal(g.tokens.cpu().numpy(), r.tokens)
+    return r
+
+
+@pytest.mark.parametrize("seed,tau_add,B,L,k,mw", [
+    (0, 0.1, 8, 48, 3, 256), (1, 0.3, 8, 48, 3, 24), (2, 1.0, 8, 32, 2, 256),
+    (3, 0.5, 4, 32, 5, 12), (4, 0.1, 16, 64, 7, 256), (5, 0.1, 32, 256, 3, 256)])
+def test_d2f_toy(mods, seed, tau_add, B, L, k, mw):
+    r = _compare(mods, seed, 64, L, B, k, tau_add, 0.95, 0.9, mw, extras=1)
+    if tau_add < 1.0:
+        assert r.max_active >= 2
+
+
+def test_d2f_dream_vocab(mods):
+    """Dream vocabulary (V=151936), GSM8K D2F parameters (Appendix table, PAPER.md:528:
+    block 32, tau_add 0.1, tau_act 0.95, tau_conf 0.90) with k=7, 3 blocks: windows up to 96."""
+    r = _compare(mods, 7, 151936, 96, 32, 7, 0.1, 0.95, 0.9, 256, extras=0)
+    assert max(w[1] for w in r.windows) > 64

@@ -397,10 +397,15 @@ def test_invalid_args_raise(L):
     with pytest.raises(L.LopaError):
         L.confidence(t[:, 1:])            # misaligned base
     with pytest.raises(L.LopaError):
-        L.Stepper(64, 65, 2, 1, 0.9, DEV).step(torch.zeros((2, 65, 64), dtype=torch.bfloat16, device=DEV),
-                                                torch.ones(1, dtype=torch.int32, device=DEV),
-                                                torch.zeros((2, 65), dtype=torch.int32, device=DEV),
-                                                torch.ones((2, 65), dtype=torch.uint8, device=DEV))
+        L.Stepper(64, 257, 2, 1, 0.9, DEV).step(torch.zeros((2, 257, 64), dtype=torch.bfloat16, device=DEV),
+                                                 torch.ones(1, dtype=torch.int32, device=DEV),
+                                                 torch.zeros((2, 257), dtype=torch.int32, device=DEV),
+                                                 torch.ones((2, 257), dtype=torch.uint8, device=DEV))
+    with pytest.raises(L.LopaError):      # W > 64 needs V <= 2^22 (R24)
+        L.Stepper((1 << 22) + 8, 65, 1, 1, 0.9, DEV).step(
+            torch.zeros((1, 65, (1 << 22) + 8), dtype=torch.bfloat16, device=DEV),
+            torch.ones(1, dtype=torch.int32, device=DEV), torch.zeros((1, 65), dtype=torch.int32, device=DEV),
+            torch.ones((1, 65), dtype=torch.uint8, device=DEV))
     with pytest.raises(L.LopaError):
         L.confidence(torch.zeros((2, 64)))  # CPU tensor: no fallback
 
@@ -506,3 +511,61 @@ def test_step_with_metric_variants(L, metric, param):
     for seed in range(20):
         _run_steps(L, seed, 64, 8, 2, 0.9, 20, extras=1, metric=metric, param=param)
     _run_steps(L, 1, 151936, 32, 7, 0.9, 2, extras=0, metric=metric, param=param)
+
+
+# ----------------------------------------------------------------------------- wide windows (D2F)
+@pytest.mark.parametrize("W", [65, 96, 128, 200, 256])
+def test_decisions_wide_windows(L, W):
+    """W > 64 (the D2F multi-block window, 8 positions per lane): Eq. 1 with per-position tau,
+    top-k spawn and Eq. 2 (all metrics) vs the oracle on random maps with forced ties."""
+    rng = np.random.default_rng(W)
+    for it in range(20):
+        conf = rng.choice(np.float32([0.1, 0.5, 0.9, 0.95]), size=W) if it % 3 == 0 \
+            else rng.random(W).astype(np.float32)
+        mask = (rng.random(W) < 0.7).astype(np.uint8)
+        if not mask.any():
+            mask[0] = 1
+        amax = rng.integers(0, 151936, size=W).astype(np.int32)
+        tok = rng.integers(0, 151936, size=W).astype(np.int32)
+        taus = rng.choice(np.float32([0.9, 0.95, 0.5]), size=W).astype(np.float32)
+        k = int(rng.integers(0, 32))
+        d = [torch.from_numpy(a).to(DEV) for a in (conf, amax, tok, mask)]
+        t, m, st = L.anchor_fill(*d, 0.9, tau_pos=torch.from_numpy(taus).to(DEV))
+        ref = O.anchor_fill(conf.astype(np.float64), amax, tok, mask, taus)
+        assert np.array_equal(t.cpu().numpy(), ref.tokens) and np.array_equal(m.cpu().numpy(), ref.mask)
+        bt, bm, look, nb = L.spawn_branches(d[0], d[1], t, m, k)
+        sp = O.spawn_branches(conf.astype(np.float64), amax, ref.tokens, ref.mask, k)
+        n = len(sp.lookahead)
+        assert int(nb.item()) == n + 1 and look.cpu().tolist()[:n] == sp.lookahead
+        assert np.array_equal(bt.cpu().numpy()[: n + 1], sp.tokens)
+        assert np.array_equal(bm.cpu().numpy()[: n + 1], sp.mask)
+        nbr = int(rng.integers(1, 17))
+        bc = rng.random((nbr, W)).astype(np.float32)
+        bmask = (rng.random((nbr, W)) < 0.5).astype(np.uint8)
+        for metric, param in ((0, 0.0), (1, 5.0), (2, 0.3)):
+            s, w = L.verify_select(torch.from_numpy(bc).to(DEV), torch.from_numpy(bmask).to(DEV),
+                                   torch.tensor([nbr], dtype=torch.int32, device=DEV), metric=metric, param=param)
+            rs = [float(np.float32(O.branch_score(bc[j].astype(np.float64), bmask[j], metric, param))) for j in range(nbr)]
+            assert s.cpu().tolist() == rs and int(w.item()) == O.verify_select(rs)
+
+
+@pytest.mark.parametrize("V,W,k", [(64, 96, 5), (1000, 128, 7), (151936, 128, 7), (64, 256, 15)])
+def test_step_wide_windows(L, V, W, k):
+    """Fused steps on W > 64 windows with per-position thresholds (tau_act on the newest block,
+    tau_conf elsewhere), iterated, against the oracle."""
+    taus = np.full(W, 0.9, np.float32)
+    taus[-32:] = 0.95
+    tp = torch.from_numpy(taus).to(DEV)
+    st = L.Stepper(V, W, k + 1, k, 0.9, DEV, tau_pos=tp)
+    tok, msk, nb = G.fresh_tables(k, W, DEV)
+    for it in range(3 if V > 10000 else 12):
+        n = int(nb.item())
+        logits = torch.zeros((k + 1, W, st.ld), dtype=torch.bfloat16, device=DEV)
+        L.syn_generate(2, 0, V, tok, msk, n_branches=n, extras=1 if V < 10000 else 0, out=logits[:n])
+        out = st.step(logits, nb, tok, msk)
+        torch.cuda.synchronize()
+        G.check_step(out, G.to_np_u16(logits), tok.cpu().numpy(), msk.cpu().numpy(), n, k, taus,
+                     vocab=V)
+        if int(out.n_next.item()) == 0:
+            break
+        tok, msk, nb = out.next_tokens.clone(), out.next_mask.clone(), out.n_next.clone()

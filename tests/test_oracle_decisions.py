@@ -204,3 +204,27 @@ def test_metric_variants_reduce_and_bound(seed):
     # ordering
     assert min(vals) <= O.branch_score(conf, mask, O.METRIC_SLIDING_MIN, w) <= max(vals)
     assert min(vals) <= O.branch_score(conf, mask, O.METRIC_BOTTOM_FRACTION, eta) <= mean + 1e-15
+
+
+# ----------------------------------------------------------------------------- per-position tau
+@pytest.mark.parametrize("seed", range(40))
+def test_per_position_tau_equals_blockwise_brute(seed):
+    """Eq. 1 with a per-position threshold (D2F window, R25) equals the literal set-builder with
+    each position's own tau (brute force), and reduces to the scalar rule for a constant map."""
+    rng = random.Random(seed)
+    W = rng.randint(1, 40)
+    conf = np.array([float(np.float32(rng.choice([0.5, 0.9, 0.95, rng.random()]))) for _ in range(W)])
+    mask = np.array([rng.random() < 0.7 for _ in range(W)], dtype=np.uint8)
+    if not mask.any():
+        mask[rng.randrange(W)] = 1
+    taus = np.array([float(np.float32(rng.choice([0.9, 0.95, 0.7]))) for _ in range(W)])
+    d = O.select_fill_set(conf, mask, taus)
+    M = [i for i in range(W) if mask[i]]
+    high = {i for i in M if conf[i] > taus[i]}
+    if high:
+        assert set(d.i_fill) == high and not d.fallback
+    else:
+        best = max(conf[i] for i in M)
+        assert d.i_fill == [min(i for i in M if conf[i] == best)] and d.fallback
+    const = O.select_fill_set(conf, mask, np.full(W, 0.9))
+    assert const.i_fill == O.select_fill_set(conf, mask, 0.9).i_fill
