@@ -65,6 +65,10 @@ namespace lopa {
 #ifndef LOPA_STAGES
 #define LOPA_STAGES 3
 #endif
+// dynamic work claims the producer keeps ahead of its issued items (0, 1 or 2)
+#ifndef LOPA_CLAIM_AHEAD
+#define LOPA_CLAIM_AHEAD 2
+#endif
 #ifndef LOPA_WGS
 #define LOPA_WGS 6
 #endif
@@ -160,6 +164,12 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// A discarded L2 load: warms the address translation (and L2) for a page used later.
+__device__ __forceinline__ void touch_global(const void* p) {
+  uint32_t d;
+  asm volatile("ld.global.cg.u8 %0, [%1];" : "=r"(d) : "l"(p) : "memory");
+  (void)d;
+}
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
 
 // ------------------------------------------------------------------ segment slice reduce
@@ -469,6 +479,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
   const int nb = max(0, min(*P.n_branches, P.cap));
   cta_scores<NT, S>(T, P, nb, W, warp, lane, P.scores);
   __syncthreads();
+  if (tid == 0) TLC(22);
   TL(7);
   if (warp >= S) return;
   constexpr int kPos = 32 * S;
@@ -669,11 +680,12 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
       // unmasked rows are skipped without a copy; two claims stay in flight so the atomic's
       // latency hides behind the issue of two items.
       const bool dyn = 2 * G < n_items;
-      uint32_t p1 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
-      uint32_t p2 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
       auto maybe_issue = [&](int cur) {
         if (row_valid(cur / n_grp)) issue(cur);
       };
+#if LOPA_CLAIM_AHEAD == 2
+      uint32_t p1 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
+      uint32_t p2 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
       if (G + b < n_items) maybe_issue(G + b);
       if (dyn) {
         while (true) {
@@ -687,6 +699,29 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
           maybe_issue(c2);
         }
       }
+#elif LOPA_CLAIM_AHEAD == 1
+      uint32_t p1 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
+      if (G + b < n_items) maybe_issue(G + b);
+      if (dyn) {
+        while (true) {
+          const int c1 = 2 * G + (int)p1;
+          if (c1 >= n_items) break;
+          p1 = atomicAdd(&P.ctrs[0], 1u);
+          maybe_issue(c1);
+        }
+      }
+#else
+      // claim only once a stage is free: no item is committed to this CTA before it can start
+      if (G + b < n_items) maybe_issue(G + b);
+      if (dyn) {
+        while (true) {
+          if (i >= (uint32_t)kStages) mbar_wait(&empty[i % kStages], ((i / kStages) - 1) & 1);
+          const int c = 2 * G + (int)atomicAdd(&P.ctrs[0], 1u);
+          if (c >= n_items) break;
+          maybe_issue(c);
+        }
+      }
+#endif
       // end-of-work sentinels: one stage per consumer phase (every warpgroup sees one)
       for (int c = 0; c < kWgStride; ++c, ++i) {
         const int s = (int)(i % kStages);
@@ -830,6 +865,25 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
       if (mine[u]) rows[pos++] = (uint16_t)(kRowsPerThread * tid + u);
   }
   const int n_masked = (int)s_wcnt[kTailThreads / 32];
+#ifndef LOPA_NO_TLB_WARM
+  // Touch the pages K1 writes and this kernel reads or writes after the wait (workspace partials,
+  // outputs) so their address translations are cached before the critical path needs them.
+  // The values loaded are discarded: nothing read here is used.
+  if (warp == kTailThreads / 32 - 1) {
+    const size_t gbytes = (size_t)P.n_grp * P.n_cand * sizeof(float4);
+    const char* gp = reinterpret_cast<const char*>(P.gpart);
+    for (size_t off = (size_t)lane * 65536; off < gbytes; off += 32 * 65536) touch_global(gp + off);
+    if (lane == 0) touch_global(P.conf);
+    if (lane == 1) touch_global(P.argmax);
+    if (lane == 2 && P.scores) touch_global(P.scores);
+    if (lane == 3 && P.next_tokens) touch_global(P.next_tokens);
+    if (lane == 4 && P.next_mask) touch_global(P.next_mask);
+    if (lane == 5 && P.lookahead) touch_global(P.lookahead);
+    if (lane == 6 && P.winner) touch_global(P.winner);
+    if (lane == 7 && P.n_next) touch_global(P.n_next);
+    if (lane == 8) touch_global(P.dev_status);
+  }
+#endif
   __syncthreads();
   grid_dep_wait();  // K1's group partials are visible from here on
   if (tid == 0) { TL(6); TLC(16); }
@@ -837,6 +891,14 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   for (int rc = tid; rc < n_masked; rc += kTailThreads) {
     const int row = rows[rc];
     const FoldAcc f = fold_row_global(P.gpart + row, n_grp, (size_t)P.n_cand);
+    if (rc == 0) TLC(17);
+#ifdef LOPA_TIMELINE
+    if (rc == 0) {  // the same loads again (now certainly L2-resident): their latency alone
+      const FoldAcc f2 = fold_row_global(P.gpart + row, n_grp, (size_t)P.n_cand);
+      if (f2.S == 12345.f) P.conf[row] = 0.f;
+      TLC(21);
+    }
+#endif
     const float c = __fdiv_rn(1.0f, f.S);
     P.conf[row] = c;
     P.argmax[row] = (int32_t)f.a;
@@ -844,6 +906,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
     T.conf[row] = c;
     T.amax[row] = (int32_t)f.a;
   }
+  if (tid == 0) TLC(18);
   __syncthreads();
   if (tid == 0) { TL(7); TLC(19); }
   if (MODE == MODE_STEP) cta_tail_step<kTailThreads, S>(P, T, tid);
@@ -1041,6 +1104,11 @@ static int ensure_kernel_attrs(int device) {
       cudaFuncSetAttribute(lopa_tail_kernel<MODE_BP_LOCAL, 8>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess)
     return LOPA_ERR_CUDA;
+#ifdef LOPA_CARVEOUT
+  cudaFuncSetAttribute(lopa_reduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, LOPA_CARVEOUT);
+  cudaFuncSetAttribute(lopa_tail_kernel<MODE_STEP, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, LOPA_CARVEOUT);
+  cudaFuncSetAttribute(lopa_tail_kernel<MODE_STEP, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, LOPA_CARVEOUT);
+#endif
   std::lock_guard<std::mutex> lk(g_mu);
   if (device >= 0 && device < 64) g_attr[device] = true;
   return LOPA_OK;

@@ -23,8 +23,9 @@ for rep in range(int(os.environ.get('REPS', 3))):
     rel = (a - t0) / 1000.0
     names = ["cta_start", "producer", "first_data", "cons_exit", "k1_cta_end", "k2_end",
              "k2_start", "k2_folded", "gp_loaded", "anchored", "gp_bar", "rows_folded", "sp_rank", "sp_write", "prod_done", "fold_bar"]
-    c = a[0, 16:21]
-    print(f"rep {rep}: rows={rows} k2_smid={int(a[0, 21])} k2 clk deltas (wait->loaded, ->folded, ->loopend, ->end):", list(np.diff(c)), "2nd fold pass", int(a[0, 22] - a[0, 18]), "raw ns k2_start", int(a[0, 6]) % 100000)
+    c = a[0]
+    print(f"rep {rep}: rows={rows} k2 clocks after wait: row0 folded {c[17]-c[16]}, loop end {c[18]-c[16]}, "
+          f"reload {c[21]-c[17]}, fold barrier {c[19]-c[16]}, scores barrier {c[22]-c[16]}, end {c[20]-c[16]}")
     for j, nm in enumerate(names):
         col = rel[:, j]
         col = col[(a[:, j] > 0) & (a[:, j] >= t0)]
