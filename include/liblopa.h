@@ -253,6 +253,27 @@ int lopa_syn_generate(uint64_t seed, int32_t block, int32_t vocab, int64_t ld, i
                       int32_t n_branches, const int32_t* branch_tokens,
                       const uint8_t* branch_mask, int32_t extras, void* out, void* stream);
 
+/* NEXT-4 — the LM-head projection with Conf fused into its epilogue: the logits
+ * never reach HBM.  For each row r of the hidden states (the rows of the verify forward whose
+ * position is masked; "parallel verification", P:207 logits reuse):
+ *   logits[r][v] = sum_k hidden[r][k] * weight[v][k]     (bf16 inputs, fp32 accumulation)
+ *   conf[r]      = 1 / sum_v exp(logits[r][v] - max_v logits[r][v])     (R1, R2)
+ *   argmax[r]    = lowest v attaining the maximum                        (R3, R4)
+ * The logits are kept in fp32 (never rounded to bf16); reading R27 in DESIGN.md gives the
+ * tolerance against the exact (fp64) definition.
+ *   hidden   device bf16 [rows][ld_hidden], 16-byte aligned, ld_hidden % 8 == 0
+ *   weight   device bf16 [vocab][ld_weight] (nn.Linear layout: one row per token), same rules
+ *   rows in [1, 256]; hidden_dim a positive multiple of 64; vocab in [1, LOPA_MAX_VOCAB]
+ *   conf, argmax  device [rows]; a row whose logits are not all finite sets
+ *            LOPA_DEV_NONFINITE (conf NaN, argmax -1)
+ *   workspace   lopa_lmhead_workspace_bytes(rows) bytes of device memory (no zeroing needed)
+ * Two kernels (tcgen05 GEMM + epilogue, then a fold of the per-SM partials) on `stream`. */
+size_t lopa_lmhead_workspace_bytes(int32_t rows);
+int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, const void* weight,
+                           int64_t ld_weight, int32_t rows, int32_t hidden_dim, int32_t vocab,
+                           float* conf, int32_t* argmax, int32_t* dev_status, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

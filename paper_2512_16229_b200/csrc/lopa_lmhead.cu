@@ -1,0 +1,440 @@
+// NEXT-4: the LM-head GEMM with the confidence reduction fused into its
+// epilogue, so the logits never touch HBM.
+//
+//   logits[r][v] = sum_k hidden[r][k] * weight[v][k]          (the model's output projection)
+//   conf[r]      = 1 / sum_v exp(logits[r][v] - max_v logits[r][v])   (Conf; R1, R2)
+//   argmax[r]    = lowest v with logits[r][v] = max                    (R3, R4)
+//
+// On tcgen05 (sm_100a): one persistent CTA per SM owns a contiguous vocabulary range and
+// streams its weight rows once (TMA, SWIZZLE_128B, L2 evict_first); the hidden states (all
+// rows, <= 256) are re-read per tile from L2 (evict_last).  Accumulators live in TMEM:
+// rows = MMA M (two 128-row halves), vocab = MMA N (<= 256 per tile), K in steps of 16.
+// Warp roles: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer (one elected lane),
+// warps 2..9 epilogue (tcgen05.ld, one thread per row: an online max / exp-sum / argmax over
+// the tile's columns, carried across the CTA's tiles).  Each CTA writes one (m, s, argmax)
+// partial per row; lopa_lmhead_fold_kernel folds the per-CTA partials of a row in fixed order.
+//
+// Precision: bf16 inputs, fp32 accumulation in TMEM (the logits are never rounded to bf16);
+// the tolerance against the fp64 oracle is derived in DESIGN.md §4 (reading R27).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "liblopa.h"
+#include "lopa_internal.h"
+#include "lopa_ptx.cuh"
+
+namespace lopa {
+namespace lmh {
+
+constexpr int kBK = 64;                    // K elements per stage (= one 128-byte swizzle row)
+constexpr int kMaxRows = 256;              // two M = 128 halves
+constexpr int kMaxN = 256;                 // vocabulary columns per tile
+constexpr int kStages = 3;
+constexpr int kHalfBytes = 128 * kBK * 2;  // 16 KB: one 128-row half of A per stage
+constexpr int kABytes = 2 * kHalfBytes;
+constexpr int kBBytes = kMaxN * kBK * 2;   // 32 KB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kTmemCols = 512;
+constexpr int kMaxGrid = 256;
+constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 /*align*/ + 256;
+
+// ---- tcgen05 / TMA PTX wrappers -------------------------------------------------------------
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// D[tmem] (+)= A[smem] . B[smem]^T, both K-major, bf16 -> fp32, M = 128, N from idesc.
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Arrive on `bar` once every tcgen05 operation issued so far by this thread has completed.
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, SWIZZLE_128B (8 rows x 128 B atoms, 1024 B apart).
+//   bits [0,14) start >> 4 | [16,30) LBO >> 4 (1: unused for swizzled K-major)
+//   [32,46) SBO >> 4 = 64 (1024 B) | [46,48) version = 1 | [61,64) layout = 2 (SWIZZLE_128B)
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+  const uint64_t start = (smem_u32(p) >> 4) & 0x3FFFu;
+  return start | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// Instruction descriptor, kind::f16: D fp32 (bits [4,6) = 1), A and B bf16 ([7,10) = [10,13) = 1),
+// both K-major, N >> 3 at [17,23), M >> 4 at [24,29).
+__device__ __forceinline__ uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// 32 lanes x 32 columns of fp32 from TMEM: thread t of the warp gets row (lane base + t),
+// columns [col, col + 32).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct Args {
+  int32_t M, K, V;
+  int32_t n_half;     // ceil(M / 128)
+  int32_t n_units;    // ceil(V / 16): 16-column vocabulary units
+  float4* gpart;      // [grid][kMaxRows] per-CTA partials (m, s, argmax bits, -)
+  float* conf;
+  int32_t* argmax;
+  int32_t* dev_status;
+};
+
+// The vocabulary units of CTA b: [u0, u1) with u = floor(b * n_units / G).
+__device__ __forceinline__ void cta_range(int b, int G, int n_units, int* u0, int* u1) {
+  *u0 = (int)(((long long)b * n_units) / G);
+  *u1 = (int)(((long long)(b + 1) * n_units) / G);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    lopa_lmhead_kernel(const __grid_constant__ CUtensorMap map_a,
+                       const __grid_constant__ CUtensorMap map_b256,
+                       const __grid_constant__ CUtensorMap map_b16, const Args A) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;   // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = (int)gridDim.x, b = (int)blockIdx.x;
+  const int n_half = A.n_half;
+  const int n_acc = n_half == 1 ? 2 : 1;  // accumulator buffers (512 TMEM columns in total)
+  int u0, u1;
+  cta_range(b, G, A.n_units, &u0, &u1);
+  const int n_tiles = (u1 - u0 + 15) / 16;
+  const int nk = A.K / kBK;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer
+      const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
+      uint32_t it = 0;
+      for (int t = 0; t < n_tiles; ++t) {
+        const int v0 = (u0 + 16 * t) * 16;
+        const int N = min(16, u1 - u0 - 16 * t) * 16;
+        const uint32_t bytes = (uint32_t)(n_half * kHalfBytes + N * kBK * 2);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = (int)(it % kStages);
+          if (it >= (uint32_t)kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+          uint8_t* sa = smem + (size_t)s * kStageBytes;
+          uint8_t* sb = sa + kABytes;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          for (int h = 0; h < n_half; ++h)
+            tma_load_2d(sa + h * kHalfBytes, &map_a, kb * kBK, h * 128, &full[s], pol_a);
+          if (N == kMaxN) {
+            tma_load_2d(sb, &map_b256, kb * kBK, v0, &full[s], pol_b);
+          } else {
+            for (int j = 0; j < N / 16; ++j)
+              tma_load_2d(sb + j * 16 * kBK * 2, &map_b16, kb * kBK, v0 + 16 * j, &full[s], pol_b);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer
+    uint32_t it = 0;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int N = min(16, u1 - u0 - 16 * t) * 16;
+      const int a = t % n_acc;
+      if (t >= n_acc) mbar_wait(&tempty[a], ((t / n_acc) - 1) & 1);
+      tc_fence_after();
+      const uint32_t idesc = idesc_bf16(128, N);
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = (int)(it % kStages);
+        mbar_wait(&full[s], (it / kStages) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint8_t* sa = smem + (size_t)s * kStageBytes;
+          const uint8_t* sb = sa + kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t bdesc = smem_desc_sw128(sb + kk * 32);
+            for (int h = 0; h < n_half; ++h) {
+              const uint64_t adesc = smem_desc_sw128(sa + h * kHalfBytes + kk * 32);
+              mma_bf16(tmem + (uint32_t)((a * n_half + h) * kMaxN), adesc, bdesc, idesc,
+                       (kb | kk) != 0 ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mma_commit(&tfull[a]);  // accumulator complete
+      __syncwarp();
+    }
+  } else {
+    // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 of half (w - 2) / 4
+    const int ew = warp - 2;
+    const int half = ew >> 2;
+    const int q = warp & 3;
+    const int row = half * 128 + q * 32 + lane;
+    const bool active = half < n_half;
+    float m = -INFINITY, ssum = 0.f;
+    int am = 0x7FFFFFFF;
+    bool bad = false;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int v0 = (u0 + 16 * t) * 16;
+      const int N = min(16, u1 - u0 - 16 * t) * 16;
+      const int a = t % n_acc;
+      mbar_wait(&tfull[a], (t / n_acc) & 1);
+      tc_fence_after();
+      if (active) {
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((a * n_half + half) * kMaxN);
+        for (int c0 = 0; c0 < N; c0 += 32) {
+          float v[32];
+          tmem_ld32(base + (uint32_t)c0, v);
+          // columns past the tile (N % 32 == 16) or past V are not logits of this tile: skipped
+          const int nv = min(min(32, N - c0), A.V - (v0 + c0));
+          float cm = -INFINITY;
+          int ci = 0x7FFFFFFF;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (i < nv) {
+              bad |= !(fabsf(v[i]) <= 3.402823466e38f);
+              if (v[i] > cm) { cm = v[i]; ci = v0 + c0 + i; }
+            }
+          }
+          if (cm > m) {
+            ssum = (m == -INFINITY) ? 0.f : ssum * ex2((m - cm) * kLog2e);
+            m = cm;
+            am = ci;
+          }
+          float cs = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < nv) cs += ex2((v[i] - m) * kLog2e);
+          ssum += cs;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+    }
+    if (active && row < A.M) {
+      if (bad) m = NAN;
+      A.gpart[(size_t)b * kMaxRows + row] = make_float4(m, ssum, __int_as_float(am), 0.f);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols)
+                 : "memory");
+  }
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
+// One warp per row: lane l folds the partials l, l + 32, ... in order, then a fixed butterfly.
+__global__ void __launch_bounds__(256) lopa_lmhead_fold_kernel(const Args A, int G) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int row = (int)(blockIdx.x * 8 + (threadIdx.x >> 5));
+  const int lane = threadIdx.x & 31;
+  if (row >= A.M) return;
+  float M = -INFINITY;
+  for (int p = lane; p < G; p += 32) M = fmax_nan(M, __ldcg(&A.gpart[(size_t)p * kMaxRows + row]).x);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) M = fmax_nan(M, __shfl_xor_sync(0xffffffffu, M, off));
+  float S = 0.f;
+  int am = 0x7FFFFFFF;
+  for (int p = lane; p < G; p += 32) {
+    const float4 q = __ldcg(&A.gpart[(size_t)p * kMaxRows + row]);
+    if (q.x == -INFINITY && M == -INFINITY) continue;  // empty range
+    S += q.y * ex2((q.x - M) * kLog2e);
+    if (q.x == M) am = min(am, __float_as_int(q.z));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    S += __shfl_xor_sync(0xffffffffu, S, off);
+    am = min(am, __shfl_xor_sync(0xffffffffu, am, off));
+  }
+  if (lane == 0) {
+    const bool ok = (S >= 1.0f) && !isnan(M);
+    A.conf[row] = ok ? __fdiv_rn(1.0f, S) : NAN;
+    A.argmax[row] = ok ? am : -1;
+    if (!ok) atomicOr(A.dev_status, LOPA_DEV_NONFINITE);
+  }
+}
+
+// ---- host ------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static std::once_flag once;
+  static EncodeTiledFn fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 map over [rows][cols] (row pitch ld elements), box = 64 columns x box_rows rows.
+static bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                     int box_rows) {
+  EncodeTiledFn f = encode_fn();
+  if (!f) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int grid_for(int device) {
+  const int n = num_sms(device);
+  return n < kMaxGrid ? n : kMaxGrid;
+}
+
+}  // namespace lmh
+}  // namespace lopa
+
+using namespace lopa;
+
+extern "C" size_t lopa_lmhead_workspace_bytes(int32_t rows) {
+  (void)rows;
+  return (size_t)lmh::kMaxGrid * lmh::kMaxRows * sizeof(float4);
+}
+
+extern "C" int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, const void* weight,
+                                      int64_t ld_weight, int32_t rows, int32_t hidden_dim,
+                                      int32_t vocab, float* conf, int32_t* argmax,
+                                      int32_t* dev_status, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  if (!hidden || !weight || !conf || !argmax || !dev_status || !workspace) return LOPA_ERR_INVALID_ARG;
+  if (rows < 1 || rows > lmh::kMaxRows || vocab < 1 || vocab > LOPA_MAX_VOCAB || hidden_dim < lmh::kBK ||
+      hidden_dim % lmh::kBK != 0)
+    return LOPA_ERR_INVALID_ARG;
+  if (ld_hidden < hidden_dim || ld_weight < hidden_dim || ld_hidden % 8 || ld_weight % 8)
+    return LOPA_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(hidden) | reinterpret_cast<uintptr_t>(weight)) & 15)
+    return LOPA_ERR_INVALID_ARG;
+  if (workspace_bytes < lopa_lmhead_workspace_bytes(rows)) return LOPA_ERR_INVALID_ARG;
+  int device = -1;
+  if (!bind_device(stream, hidden, &device)) return LOPA_ERR_CUDA;
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (major != 10 || minor != 0) return LOPA_ERR_UNSUPPORTED;
+  CUtensorMap ma, mb256, mb16;
+  if (!lmh::make_map(&ma, hidden, rows, hidden_dim, ld_hidden, 128) ||
+      !lmh::make_map(&mb256, weight, vocab, hidden_dim, ld_weight, 256) ||
+      !lmh::make_map(&mb16, weight, vocab, hidden_dim, ld_weight, 16))
+    return LOPA_ERR_CUDA;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] {
+    attr_err = cudaFuncSetAttribute(lmh::lopa_lmhead_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lmh::kSmemBytes);
+  });
+  if (attr_err != cudaSuccess) return LOPA_ERR_CUDA;
+  lmh::Args a;
+  a.M = rows;
+  a.K = hidden_dim;
+  a.V = vocab;
+  a.n_half = (rows + 127) / 128;
+  a.n_units = (vocab + 15) / 16;
+  a.gpart = static_cast<float4*>(workspace);
+  a.conf = conf;
+  a.argmax = argmax;
+  a.dev_status = dev_status;
+  const int G = lmh::grid_for(device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  lmh::lopa_lmhead_kernel<<<G, lmh::kThreads, lmh::kSmemBytes, s>>>(ma, mb256, mb16, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return LOPA_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((rows + 7) / 8);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, lmh::lopa_lmhead_fold_kernel, a, G);
+  return e == cudaSuccess ? LOPA_OK : LOPA_ERR_CUDA;
+}

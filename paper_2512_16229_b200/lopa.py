@@ -88,6 +88,9 @@ _SIGS = {
     "lopa_profile_read": (_i32, [ctypes.POINTER(ctypes.c_float), _i32, ctypes.POINTER(_i32)]),
     "lopa_syn_generate": (_i32, [_u64, _i32, _i32, _i64, _i32, _i32, _c_void_p, _c_void_p, _i32,
                                  _c_void_p, _c_void_p]),
+    "lopa_lmhead_workspace_bytes": (_size, [_i32]),
+    "lopa_lmhead_confidence": (_i32, [_c_void_p, _i64, _c_void_p, _i64, _i32, _i32, _i32, _c_void_p,
+                                      _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -174,6 +177,39 @@ def confidence(logits: torch.Tensor, vocab: int | None = None, row_mask: torch.T
                                  _p(status), _p(workspace), workspace.numel(), _stream(dev)),
            "lopa_confidence")
     return conf, amax, status
+
+
+# ----------------------------------------------------------------------------- NEXT-4
+class LMHead:
+    """LM-head projection with Conf fused into the GEMM epilogue (tcgen05): conf / argmax of
+    each row of ``hidden`` (bf16 [rows][K]) against ``weight`` (bf16 [V][K]) without
+    materialising the logits.  Owns its workspace; rows <= 256, K % 64 == 0."""
+
+    def __init__(self, weight: torch.Tensor, max_rows: int = 256):
+        _need_cuda(weight)
+        if weight.dtype != torch.bfloat16 or weight.dim() != 2 or weight.stride(1) != 1:
+            raise LopaError("weight must be a 2-D bf16 tensor [V][K] with unit inner stride")
+        self.weight = weight
+        self.vocab, self.hidden_dim = weight.shape
+        dev = weight.device
+        self.ws = torch.empty(lib().lopa_lmhead_workspace_bytes(max_rows), dtype=torch.uint8, device=dev)
+        self.status = new_status(dev)
+        self.conf = torch.empty(max_rows, dtype=torch.float32, device=dev)
+        self.argmax = torch.empty(max_rows, dtype=torch.int32, device=dev)
+
+    def __call__(self, hidden: torch.Tensor):
+        _need_cuda(hidden)
+        if hidden.dtype != torch.bfloat16 or hidden.dim() != 2 or hidden.stride(1) != 1:
+            raise LopaError("hidden must be a 2-D bf16 tensor [rows][K] with unit inner stride")
+        rows = hidden.shape[0]
+        if hidden.shape[1] != self.hidden_dim or rows > self.conf.numel():
+            raise LopaError("hidden shape does not match the weight / max_rows")
+        _check(lib().lopa_lmhead_confidence(_p(hidden), hidden.stride(0), _p(self.weight),
+                                            self.weight.stride(0), rows, self.hidden_dim, self.vocab,
+                                            _p(self.conf), _p(self.argmax), _p(self.status),
+                                            _p(self.ws), self.ws.numel(), _stream(hidden.device)),
+               "lopa_lmhead_confidence")
+        return self.conf[:rows], self.argmax[:rows], self.status
 
 
 # ----------------------------------------------------------------------------- a3

@@ -165,3 +165,32 @@ def bf16_bits_to_f32(u16: np.ndarray) -> np.ndarray:
 def fresh_block(window: int):
     """A fully masked block: tokens all 0, mask all 1."""
     return np.zeros(window, dtype=np.int32), np.ones(window, dtype=np.uint8)
+
+
+# ----------------------------------------------------------------------------- LM-head inputs
+def _f32_to_bf16_rne(x: np.ndarray) -> np.ndarray:
+    """float32 -> bf16 bits, round to nearest even (inputs only; finite values)."""
+    u = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return r.astype(np.uint16)
+
+
+def lmhead_inputs(seed: int, rows: int, hidden_dim: int, vocab: int, sigma: float = 1.5,
+                  spike_lo: float = 4.0, spike_hi: float = 16.0, chunk: int = 8192):
+    """Seeded SYN-LMH inputs: weight W [V][K] ~ N(0, 1/K) (rows of norm ~1, the
+    scale of a trained output projection), hidden rows h_r = sigma·z + beta_r·W[t_r]/|W[t_r]|^2
+    with a planted target token t_r and logit margin beta_r ~ U[spike_lo, spike_hi], so the
+    logit of t_r sits ~beta_r above a N(0, sigma^2) background: conf spans ~1e-4 .. 0.99 at
+    V = 151936.  Returns (hidden bf16 bits [rows][K], weight bf16 bits [V][K], targets)."""
+    rng = np.random.default_rng(seed)
+    W = np.empty((vocab, hidden_dim), dtype=np.uint16)
+    for v0 in range(0, vocab, chunk):
+        n = min(chunk, vocab - v0)
+        W[v0:v0 + n] = _f32_to_bf16_rne(rng.standard_normal((n, hidden_dim), dtype=np.float32)
+                                        / np.float32(math.sqrt(hidden_dim)))
+    t = rng.integers(0, vocab, size=rows)
+    beta = rng.uniform(spike_lo, spike_hi, size=rows)
+    Wt = bf16_bits_to_f32(W[t]).astype(np.float64)
+    z = rng.standard_normal((rows, hidden_dim))
+    h = sigma * z + (beta / (Wt * Wt).sum(axis=1))[:, None] * Wt
+    return _f32_to_bf16_rne(h.astype(np.float32)), W, t

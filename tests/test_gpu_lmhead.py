@@ -1,0 +1,95 @@
+"""GPU parity of the fused LM-head + Conf kernel (NEXT-4, lopa_lmhead_confidence) against the
+fp64 oracle (oracle/lmhead_oracle.py) on seeded SYN-LMH inputs.  Tolerance (R27): per row,
+|conf - conf_ref| <= conf_ref·(exp(2E_r) - 1) + 2e-6 with E_r the fp32-accumulation bound;
+argmax exact unless the oracle's top-2 logit gap is below 2E_r (then it must be one of the
+tokens within 2E_r of the max)."""
+import numpy as np
+import pytest
+import torch
+
+import syngen
+from oracle import lmhead_oracle as LO
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2512_16229_b200 import lopa
+    return lopa
+
+
+def _dev(u16):
+    return torch.from_numpy(np.ascontiguousarray(u16).view(np.int16)).to(DEV).view(torch.bfloat16)
+
+
+def _check(L, h, W, rows=None, stats=None):
+    head = L.LMHead(_dev(W))
+    c, a, st = head(_dev(h))
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    g_c = c.cpu().numpy().astype(np.float64)
+    g_a = a.cpu().numpy()
+    sel = np.arange(h.shape[0]) if rows is None else np.asarray(rows)
+    rc, ra, ok, Lg = LO.lmhead_confidence(h, W, sel)
+    E = LO.logit_error_bound(h, W, sel)
+    assert ok.all()
+    for i, r in enumerate(sel):
+        tol = rc[i] * np.expm1(2 * E[i]) + 2e-6
+        assert abs(g_c[r] - rc[i]) <= tol, (r, g_c[r], rc[i], tol)
+        srt = np.sort(Lg[i])[::-1]
+        if srt.size > 1 and srt[0] - srt[1] < 2 * E[i]:
+            assert Lg[i][g_a[r]] >= srt[0] - 2 * E[i]
+        else:
+            assert g_a[r] == ra[i], (r, g_a[r], ra[i])
+        if stats is not None:
+            stats.append(abs(g_c[r] - rc[i]) / rc[i])
+    return g_c, g_a
+
+
+@pytest.mark.parametrize("M,K,V", [(1, 64, 16), (7, 64, 100), (33, 128, 1000), (128, 256, 4096),
+                                   (129, 64, 8200), (200, 192, 4111), (256, 128, 16),
+                                   (256, 320, 5000), (64, 3584, 2048)])
+def test_lmhead_shapes(L, M, K, V):
+    h, W, _ = syngen.lmhead_inputs(M * 7 + V, M, K, V)
+    st = []
+    _check(L, h, W, stats=st)
+    assert np.mean(st) < 1e-4     # far inside the worst-case bound in practice
+
+
+def test_lmhead_dream_size(L):
+    """Dream-7B shapes: V = 151936 tokens, K = 3584, the 241 masked rows of the bench step;
+    32 sampled rows against the oracle, plus every row's argmax against the planted token
+    where the planted margin is large."""
+    M, K, V = 241, 3584, 151936
+    h, W, t = syngen.lmhead_inputs(2024, M, K, V)
+    rows = list(range(0, M, 8)) + [M - 1]
+    _check(L, h, W, rows=rows)
+
+
+def test_lmhead_nonfinite(L):
+    h, W, _ = syngen.lmhead_inputs(1, 4, 64, 300)
+    h = h.copy()
+    h[2, 5] = 0x7FC0   # NaN
+    head = L.LMHead(_dev(W))
+    c, a, st = head(_dev(h))
+    torch.cuda.synchronize()
+    assert int(st.item()) & L.DEV_NONFINITE
+    assert int(a[2].item()) == -1 and np.isnan(float(c[2].item()))
+    rc, ra, ok, _ = LO.lmhead_confidence(h, W, [0, 1, 3])
+    assert a.cpu().numpy()[[0, 1, 3]].tolist() == ra.tolist()
+
+
+def test_lmhead_repeatable(L):
+    """Same inputs -> bit-identical outputs (fixed vocabulary split and fold order)."""
+    h, W, _ = syngen.lmhead_inputs(77, 100, 256, 20000)
+    head = L.LMHead(_dev(W))
+    hd = _dev(h)
+    c1, a1, _ = head(hd)
+    c1, a1 = c1.clone(), a1.clone()
+    for _ in range(3):
+        c2, a2, _ = head(hd)
+        assert torch.equal(c1, c2) and torch.equal(a1, a2)
