@@ -42,9 +42,11 @@ def logits(hidden_u16, weight_u16, rows=None, chunk: int = 16384) -> np.ndarray:
 
 def conf_from_logits(l):
     """Conf / greedy token of one row of exact logits (R1, R2, R4).  Returns
-    (conf, argmax, ok); a row with a non-finite logit is not a distribution (ok = False)."""
+    (conf, argmax, ok).  As for rows of bf16 logits (R20): a row with a NaN or +inf logit,
+    or whose logits are all -inf, is not a distribution (ok = False); a -inf logit is a
+    token of probability 0."""
     l = np.asarray(l, dtype=np.float64)
-    if not np.all(np.isfinite(l)):
+    if np.isnan(l).any() or np.isposinf(l).any() or np.isneginf(l).all():
         return float("nan"), -1, False
     m = l.max()
     return float(1.0 / np.exp(l - m).sum()), int(np.argmax(l)), True

@@ -38,11 +38,12 @@ constexpr int kHalfBytes = 128 * kBK * 2;  // 16 KB: one 128-row half of A per s
 constexpr int kABytes = 2 * kHalfBytes;
 constexpr int kBBytes = kMaxN * kBK * 2;   // 32 KB
 constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kTmemCols = 512;
 constexpr int kMaxGrid = 256;
-constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 /*align*/ + 256;
+constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 /*align*/ + 256 +
+                              kMaxRows * 16 /*row exchange*/;
 
 // ---- tcgen05 / TMA PTX wrappers -------------------------------------------------------------
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
@@ -117,6 +118,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Optional wait-time accounting (-DLOPA_LMH_PROF): clock64 cycles each role spends waiting,
+// per CTA, read back with lopa_debug_lmhead_prof().  Compiled out of the product build.
+#ifdef LOPA_LMH_PROF
+__device__ unsigned long long g_lmh_prof[kMaxGrid * 8];
+#define LMH_T0() const long long _t0 = clock64()
+#define LMH_ACC(slot) atomicAdd(&g_lmh_prof[blockIdx.x * 8 + (slot)], (unsigned long long)(clock64() - _t0))
+#else
+#define LMH_T0() ((void)0)
+#define LMH_ACC(slot) ((void)0)
+#endif
+
 struct Args {
   int32_t M, K, V;
   int32_t n_half;     // ceil(M / 128)
@@ -145,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kStages;   // [2]
   uint64_t* tempty = tfull + 2;        // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float4* xch = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 256);  // [kMaxRows]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = (int)gridDim.x, b = (int)blockIdx.x;
@@ -154,6 +167,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   cta_range(b, G, A.n_units, &u0, &u1);
   const int n_tiles = (u1 - u0 + 15) / 16;
   const int nk = A.K / kBK;
+#ifdef LOPA_LMH_PROF
+  if (tid == 0) g_lmh_prof[blockIdx.x * 8 + 6] = (unsigned long long)clock64();
+#endif
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -189,7 +205,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t bytes = (uint32_t)(n_half * kHalfBytes + N * kBK * 2);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = (int)(it % kStages);
-          if (it >= (uint32_t)kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+          {
+            LMH_T0();
+            if (it >= (uint32_t)kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+            LMH_ACC(0);
+          }
           uint8_t* sa = smem + (size_t)s * kStageBytes;
           uint8_t* sb = sa + kABytes;
           mbar_arrive_expect_tx(&full[s], bytes);
@@ -210,12 +230,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0; t < n_tiles; ++t) {
       const int N = min(16, u1 - u0 - 16 * t) * 16;
       const int a = t % n_acc;
-      if (t >= n_acc) mbar_wait(&tempty[a], ((t / n_acc) - 1) & 1);
+      {
+        LMH_T0();
+        if (t >= n_acc) mbar_wait(&tempty[a], ((t / n_acc) - 1) & 1);
+        if (lane == 0) LMH_ACC(1);
+      }
       tc_fence_after();
       const uint32_t idesc = idesc_bf16(128, N);
       for (int kb = 0; kb < nk; ++kb, ++it) {
         const int s = (int)(it % kStages);
-        mbar_wait(&full[s], (it / kStages) & 1);
+        {
+          LMH_T0();
+          mbar_wait(&full[s], (it / kStages) & 1);
+          if (lane == 0) LMH_ACC(2);
+        }
         tc_fence_after();
         if (lane == 0) {
           const uint8_t* sa = smem + (size_t)s * kStageBytes;
@@ -237,58 +265,93 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     }
   } else {
-    // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 of half (w - 2) / 4
+    // ---- epilogue: 16 warps; warp w reads TMEM lanes 32 (w % 4) .. +31 (hardware rule).
+    // ew = w - 2: bits 0-1 lane quarter (via w % 4), bit 2 = M half, bit 3 = column parity:
+    // a thread owns one row and the 32-column chunks of its parity of every tile.
     const int ew = warp - 2;
-    const int half = ew >> 2;
+    const int half = (ew >> 2) & 1;
+    const int par = ew >> 3;
     const int q = warp & 3;
     const int row = half * 128 + q * 32 + lane;
     const bool active = half < n_half;
     float m = -INFINITY, ssum = 0.f;
     int am = 0x7FFFFFFF;
-    bool bad = false;
     for (int t = 0; t < n_tiles; ++t) {
       const int v0 = (u0 + 16 * t) * 16;
       const int N = min(16, u1 - u0 - 16 * t) * 16;
       const int a = t % n_acc;
-      mbar_wait(&tfull[a], (t / n_acc) & 1);
+      {
+        LMH_T0();
+        mbar_wait(&tfull[a], (t / n_acc) & 1);
+        if (lane == 0 && ew == 0) LMH_ACC(3);
+      }
+#ifdef LOPA_LMH_PROF
+      const long long _te = clock64();
+#endif
       tc_fence_after();
       if (active) {
         const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((a * n_half + half) * kMaxN);
-        for (int c0 = 0; c0 < N; c0 += 32) {
+        for (int c0 = 32 * par; c0 < N; c0 += 64) {
           float v[32];
           tmem_ld32(base + (uint32_t)c0, v);
-          // columns past the tile (N % 32 == 16) or past V are not logits of this tile: skipped
+          // columns past the tile (N % 32 == 16) or past V are not logits: exp(-inf) = 0
           const int nv = min(min(32, N - c0), A.V - (v0 + c0));
-          float cm = -INFINITY;
-          int ci = 0x7FFFFFFF;
+          if (nv < 32) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            if (i < nv) {
-              bad |= !(fabsf(v[i]) <= 3.402823466e38f);
-              if (v[i] > cm) { cm = v[i]; ci = v0 + c0 + i; }
-            }
+            for (int i = 0; i < 32; ++i) v[i] = i < nv ? v[i] : -INFINITY;
           }
-          if (cm > m) {
+          float cm = v[0];
+#pragma unroll
+          for (int i = 1; i < 32; ++i) cm = fmax_nan(cm, v[i]);
+          if (cm == -INFINITY) continue;  // every term exp(-inf) = 0
+          if (cm > m) {  // new running maximum: its first column, and rescale the sum
+            int ci = 31;
+#pragma unroll
+            for (int i = 31; i >= 0; --i) ci = v[i] == cm ? i : ci;
             ssum = (m == -INFINITY) ? 0.f : ssum * ex2((m - cm) * kLog2e);
             m = cm;
-            am = ci;
+            am = v0 + c0 + ci;
+          } else if (cm != cm) {
+            m = cm;  // NaN: the row is not a distribution (propagates into the sum)
           }
-          float cs = 0.f;
+          float2 acc = make_float2(0.f, 0.f);
+          const float2 nm = make_float2(-m, -m), l2 = make_float2(kLog2e, kLog2e);
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < nv) cs += ex2((v[i] - m) * kLog2e);
-          ssum += cs;
+          for (int i = 0; i < 16; ++i) {
+            const float2 d = __fmul2_rn(__fadd2_rn(make_float2(v[2 * i], v[2 * i + 1]), nm), l2);
+            acc = __fadd2_rn(acc, make_float2(ex2(d.x), ex2(d.y)));
+          }
+          ssum += acc.x + acc.y;
         }
       }
       tc_fence_before();
       __syncwarp();
+#ifdef LOPA_LMH_PROF
+      if (lane == 0 && ew == 0) atomicAdd(&g_lmh_prof[blockIdx.x * 8 + 4], (unsigned long long)(clock64() - _te));
+#endif
       if (lane == 0) mbar_arrive(&tempty[a]);
     }
-    if (active && row < A.M) {
-      if (bad) m = NAN;
-      A.gpart[(size_t)b * kMaxRows + row] = make_float4(m, ssum, __int_as_float(am), 0.f);
+    // combine the two column parities of each row (fixed order: parity 0 folds parity 1 in)
+    if (par == 1) xch[row] = make_float4(m, ssum, __int_as_float(am), 0.f);
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpiWarps) : "memory");
+    if (par == 0 && active && row < A.M) {
+      const float4 o = xch[row];
+      const float M = fmax_nan(m, o.x);
+      float S = 0.f;
+      if (M == -INFINITY || M != M) {
+        S = (M != M) ? M : 0.f;
+      } else {
+        S = ssum * ex2((m - M) * kLog2e) + o.y * ex2((o.x - M) * kLog2e);
+      }
+      int best = 0x7FFFFFFF;
+      if (m == M) best = am;
+      if (o.x == M) best = min(best, __float_as_int(o.z));
+      A.gpart[(size_t)b * kMaxRows + row] = make_float4(M, S, __int_as_float(best), 0.f);
     }
   }
+#ifdef LOPA_LMH_PROF
+  if (tid == 0) g_lmh_prof[blockIdx.x * 8 + 5] = (unsigned long long)clock64();
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -372,6 +435,16 @@ static int grid_for(int device) {
 }  // namespace lopa
 
 using namespace lopa;
+
+#ifdef LOPA_LMH_PROF
+extern "C" __attribute__((visibility("default"))) int lopa_debug_lmhead_prof(unsigned long long* out, int n) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, lmh::g_lmh_prof, sizeof(unsigned long long) * n * 8);
+  static unsigned long long zeros[lmh::kMaxGrid * 8];
+  cudaMemcpyToSymbol(lmh::g_lmh_prof, zeros, sizeof(zeros));
+  return 0;
+}
+#endif
 
 extern "C" size_t lopa_lmhead_workspace_bytes(int32_t rows) {
   (void)rows;

@@ -93,3 +93,12 @@ def test_generator_shape_and_spread():
     assert h.shape == (16, 128) and W.shape == (2000, 128) and h.dtype == np.uint16
     c, a, ok, _ = LO.lmhead_confidence(h, W)
     assert ok.all() and (a == t).mean() > 0.8 and c.min() < 0.5 < c.max()
+
+
+def test_neg_inf_logits_are_zero_probability():
+    """R20 applied to exact logits: -inf entries are tokens of probability 0; only an all -inf
+    row (or NaN / +inf) is not a distribution."""
+    c, a, ok = LO.conf_from_logits(np.array([-np.inf, 1.0, 1.0, -np.inf]))
+    assert ok and a == 1 and c == 0.5
+    assert not LO.conf_from_logits(np.array([-np.inf, -np.inf]))[2]
+    assert not LO.conf_from_logits(np.array([0.0, np.inf]))[2]
