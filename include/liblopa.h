@@ -264,15 +264,29 @@ int lopa_syn_generate(uint64_t seed, int32_t block, int32_t vocab, int64_t ld, i
  *   hidden   device bf16 [rows][ld_hidden], 16-byte aligned, ld_hidden % 8 == 0
  *   weight   device bf16 [vocab][ld_weight] (nn.Linear layout: one row per token), same rules
  *   rows in [1, 256]; hidden_dim a positive multiple of 64; vocab in [1, LOPA_MAX_VOCAB]
- *   conf, argmax  device [rows]; a row whose logits are not all finite sets
- *            LOPA_DEV_NONFINITE (conf NaN, argmax -1)
+ *   row_mask device uint8 [rows] or NULL: rows with row_mask[r] == 0 get conf NaN, argmax -1
+ *   conf, argmax  device [rows]; a selected row whose logits contain NaN or +inf, or are all
+ *            -inf, sets LOPA_DEV_NONFINITE (conf NaN, argmax -1); -inf logits are tokens of
+ *            probability 0 (R20)
  *   workspace   lopa_lmhead_workspace_bytes(rows) bytes of device memory (no zeroing needed)
  * Two kernels (tcgen05 GEMM + epilogue, then a fold of the per-SM partials) on `stream`. */
 size_t lopa_lmhead_workspace_bytes(int32_t rows);
 int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, const void* weight,
                            int64_t ld_weight, int32_t rows, int32_t hidden_dim, int32_t vocab,
-                           float* conf, int32_t* argmax, int32_t* dev_status, void* workspace,
-                           size_t workspace_bytes, void* stream);
+                           const uint8_t* row_mask, float* conf, int32_t* argmax,
+                           int32_t* dev_status, void* workspace, size_t workspace_bytes,
+                           void* stream);
+
+/* The verify step of lopa_step (a1 -> a2 -> a3 -> a4) from the verify forward's HIDDEN STATES
+ * instead of its logits: a1 is the fused LM-head + Conf above over the max_branches * window
+ * rows (<= 256) of `hidden` (bf16 [max_branches][window][ld_hidden], row b * window + i =
+ * branch b, position i), restricted to the masked rows of present branches; then the same
+ * decision kernel as lopa_step.  args->logits and args->ld are ignored; every other field of
+ * `args` keeps its lopa_step meaning (conf / argmax receive the fused a1 results).
+ * lmh_workspace: lopa_lmhead_workspace_bytes(rows) bytes.  Three kernels, PDL-chained. */
+int lopa_step_lmhead(const lopa_step_args_t* args, const void* hidden, int64_t ld_hidden,
+                     const void* weight, int64_t ld_weight, int32_t hidden_dim,
+                     void* lmh_workspace, size_t lmh_workspace_bytes, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

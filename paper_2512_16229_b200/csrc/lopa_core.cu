@@ -89,7 +89,8 @@ static_assert(kConsumerWGs % kSegPerItem == 0, "warpgroups cover the segments of
 // tell consecutive phases apart), so each stage belongs to exactly one consumer phase.
 static_assert(kStages % kWgStride == 0, "stages must divide evenly among consumer phases");
 
-enum Mode : int { MODE_CONF = 0, MODE_STEP = 1, MODE_BP_LOCAL = 2 };
+enum Mode : int { MODE_CONF = 0, MODE_STEP = 1, MODE_BP_LOCAL = 2, MODE_DECIDE = 3 };
+// MODE_DECIDE: conf / argmax already in P.conf / P.argmax (the fused LM-head path); K2 only decides.
 
 struct Params {
   const uint16_t* logits;
@@ -888,6 +889,13 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   grid_dep_wait();  // K1's group partials are visible from here on
   if (tid == 0) { TL(6); TLC(16); }
   const int n_grp = P.n_grp;
+  if (MODE == MODE_DECIDE) {
+    for (int rc = tid; rc < n_masked; rc += kTailThreads) {
+      const int row = rows[rc];
+      T.conf[row] = __ldcg(P.conf + row);
+      T.amax[row] = __ldcg(P.argmax + row);
+    }
+  } else
   for (int rc = tid; rc < n_masked; rc += kTailThreads) {
     const int row = rows[rc];
     const FoldAcc f = fold_row_global(P.gpart + row, n_grp, (size_t)P.n_cand);
@@ -909,7 +917,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   if (tid == 0) TLC(18);
   __syncthreads();
   if (tid == 0) { TL(7); TLC(19); }
-  if (MODE == MODE_STEP) cta_tail_step<kTailThreads, S>(P, T, tid);
+  if (MODE == MODE_STEP || MODE == MODE_DECIDE) cta_tail_step<kTailThreads, S>(P, T, tid);
   if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads, S>(P, T, tid);
   if (tid == 0) {
     P.ctrs[0] = 0;
@@ -1102,6 +1110,10 @@ static int ensure_kernel_attrs(int device) {
       cudaFuncSetAttribute(lopa_tail_kernel<MODE_BP_LOCAL, 2>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
       cudaFuncSetAttribute(lopa_tail_kernel<MODE_BP_LOCAL, 8>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(lopa_tail_kernel<MODE_DECIDE, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(lopa_tail_kernel<MODE_DECIDE, 8>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess)
     return LOPA_ERR_CUDA;
 #ifdef LOPA_CARVEOUT
@@ -1229,9 +1241,10 @@ static bool logits_ok(const void* logits, int64_t ld, int32_t vocab) {
          (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
 }
 
-int validate_step_args(const lopa_step_args_t* a, bool need_next) {
+int validate_step_args(const lopa_step_args_t* a, bool need_next, bool need_logits) {
   if (!a) return LOPA_ERR_INVALID_ARG;
-  if (!logits_ok(a->logits, a->ld, a->vocab)) return LOPA_ERR_INVALID_ARG;
+  if (need_logits && !logits_ok(a->logits, a->ld, a->vocab)) return LOPA_ERR_INVALID_ARG;
+  if (!need_logits && (a->vocab < 1)) return LOPA_ERR_INVALID_ARG;
   if (a->window < 1 || a->max_branches < 1 || a->k < 0) return LOPA_ERR_INVALID_ARG;
   if (!(a->tau > 0.f && a->tau <= 1.f)) return LOPA_ERR_INVALID_ARG;
   if (!metric_ok(a->metric, a->metric_param)) return LOPA_ERR_INVALID_ARG;
@@ -1281,7 +1294,7 @@ static Params base_params(const lopa_step_args_t* a, const Workspace& ws) {
 
 int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_loc, void* record,
                     cudaStream_t s) {
-  int st = validate_step_args(a, false);
+  int st = validate_step_args(a, false, true);
   if (st != LOPA_OK) return st;
   if (!record || b_loc < 1 || branch_base < 0) return LOPA_ERR_INVALID_ARG;
   if (b_loc > LOPA_MAX_BRANCHES || (int64_t)b_loc * a->window > LOPA_MAX_ROWS)
@@ -1299,6 +1312,29 @@ int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_lo
   P.row_mask = a->branch_mask + (size_t)branch_base * a->window;
   P.record = static_cast<uint8_t*>(record);
   return launch_reduce(P, dev, s);
+}
+
+// a2 -> a3 -> a4 on conf / argmax already in a->conf / a->argmax (written by the previous kernel
+// on the stream: K2 is launched programmatically dependent on it).
+int launch_step_decide(const lopa_step_args_t* a, cudaStream_t s) {
+  int st = validate_step_args(a, true, false);
+  if (st != LOPA_OK) return st;
+  const int32_t rows = a->max_branches * a->window;
+  if (rows > LOPA_MAX_ROWS) return LOPA_ERR_UNSUPPORTED;
+  Workspace ws;
+  if (!carve_workspace(a->workspace, a->workspace_bytes, rows, a->vocab, &ws))
+    return LOPA_ERR_INVALID_ARG;
+  int dev;
+  if (!bind_device(s, a->conf, &dev)) return LOPA_ERR_CUDA;
+  st = ensure_kernel_attrs(dev);
+  if (st != LOPA_OK) return st;
+  Params P = base_params(a, ws);
+  P.mode = MODE_DECIDE;
+  P.cap = a->max_branches;
+  P.n_cand = rows;
+  P.row_mask = a->branch_mask;
+  auto kern = P.window > 64 ? lopa_tail_kernel<MODE_DECIDE, 8> : lopa_tail_kernel<MODE_DECIDE, 2>;
+  return cuda_status(launch_pdl(kern, dim3(1), dim3(kTailThreads), kTailSmemBytes, s, P));
 }
 
 int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, const void* records,
@@ -1523,7 +1559,7 @@ extern "C" int lopa_verify_select_ex(const float* conf, const uint8_t* branch_ma
 }
 
 extern "C" int lopa_step(const lopa_step_args_t* a, void* stream) {
-  int st = validate_step_args(a, true);
+  int st = validate_step_args(a, true, true);
   if (st != LOPA_OK) return st;
   const int32_t rows = a->max_branches * a->window;
   if (rows > LOPA_MAX_ROWS) return LOPA_ERR_UNSUPPORTED;

@@ -49,6 +49,7 @@ int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, co
                      cudaStream_t s);
 int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_loc, void* record,
                     cudaStream_t s);
-int validate_step_args(const lopa_step_args_t* a, bool need_next);
+int validate_step_args(const lopa_step_args_t* a, bool need_next, bool need_logits = true);
+int launch_step_decide(const lopa_step_args_t* a, cudaStream_t s);
 
 }  // namespace lopa

@@ -137,6 +137,9 @@ struct Args {
   float* conf;
   int32_t* argmax;
   int32_t* dev_status;
+  const uint8_t* row_mask;     // nullable: rows with row_mask[r] == 0 are not reported
+  const int32_t* n_branches;   // nullable: rows r with r / window >= *n_branches are not reported
+  int32_t window;
 };
 
 // The vocabulary units of CTA b: [u0, u1) with u = floor(b * n_units / G).
@@ -368,6 +371,14 @@ __global__ void __launch_bounds__(256) lopa_lmhead_fold_kernel(const Args A, int
   const int row = (int)(blockIdx.x * 8 + (threadIdx.x >> 5));
   const int lane = threadIdx.x & 31;
   if (row >= A.M) return;
+  const bool valid = (!A.row_mask || A.row_mask[row] != 0) && (!A.n_branches || row / A.window < *A.n_branches);
+  if (!valid) {  // not a row of the step: untouched semantics of a1 (conf NaN, argmax -1)
+    if (lane == 0) {
+      A.conf[row] = NAN;
+      A.argmax[row] = -1;
+    }
+    return;
+  }
   float M = -INFINITY;
   for (int p = lane; p < G; p += 32) M = fmax_nan(M, __ldcg(&A.gpart[(size_t)p * kMaxRows + row]).x);
 #pragma unroll
@@ -451,11 +462,10 @@ extern "C" size_t lopa_lmhead_workspace_bytes(int32_t rows) {
   return (size_t)lmh::kMaxGrid * lmh::kMaxRows * sizeof(float4);
 }
 
-extern "C" int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, const void* weight,
-                                      int64_t ld_weight, int32_t rows, int32_t hidden_dim,
-                                      int32_t vocab, float* conf, int32_t* argmax,
-                                      int32_t* dev_status, void* workspace, size_t workspace_bytes,
-                                      void* stream) {
+static int launch_lmhead(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                         int32_t rows, int32_t hidden_dim, int32_t vocab, const uint8_t* row_mask,
+                         const int32_t* n_branches, int32_t window, float* conf, int32_t* argmax,
+                         int32_t* dev_status, void* workspace, size_t workspace_bytes, void* stream) {
   if (!hidden || !weight || !conf || !argmax || !dev_status || !workspace) return LOPA_ERR_INVALID_ARG;
   if (rows < 1 || rows > lmh::kMaxRows || vocab < 1 || vocab > LOPA_MAX_VOCAB || hidden_dim < lmh::kBK ||
       hidden_dim % lmh::kBK != 0)
@@ -493,6 +503,9 @@ extern "C" int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, con
   a.conf = conf;
   a.argmax = argmax;
   a.dev_status = dev_status;
+  a.row_mask = row_mask;
+  a.n_branches = n_branches;
+  a.window = window < 1 ? 1 : window;
   const int G = lmh::grid_for(device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   lmh::lopa_lmhead_kernel<<<G, lmh::kThreads, lmh::kSmemBytes, s>>>(ma, mb256, mb16, a);
@@ -510,4 +523,28 @@ extern "C" int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, con
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, lmh::lopa_lmhead_fold_kernel, a, G);
   return e == cudaSuccess ? LOPA_OK : LOPA_ERR_CUDA;
+}
+
+extern "C" int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, const void* weight,
+                                      int64_t ld_weight, int32_t rows, int32_t hidden_dim,
+                                      int32_t vocab, const uint8_t* row_mask, float* conf,
+                                      int32_t* argmax, int32_t* dev_status, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
+  return launch_lmhead(hidden, ld_hidden, weight, ld_weight, rows, hidden_dim, vocab, row_mask,
+                       nullptr, 1, conf, argmax, dev_status, workspace, workspace_bytes, stream);
+}
+
+extern "C" int lopa_step_lmhead(const lopa_step_args_t* a, const void* hidden, int64_t ld_hidden,
+                                const void* weight, int64_t ld_weight, int32_t hidden_dim,
+                                void* lmh_workspace, size_t lmh_workspace_bytes, void* stream) {
+  if (!a) return LOPA_ERR_INVALID_ARG;
+  int st = validate_step_args(a, true, false);
+  if (st != LOPA_OK) return st;
+  const int64_t rows = (int64_t)a->max_branches * a->window;
+  if (rows > lmh::kMaxRows) return LOPA_ERR_UNSUPPORTED;
+  st = launch_lmhead(hidden, ld_hidden, weight, ld_weight, (int32_t)rows, hidden_dim, a->vocab,
+                     a->branch_mask, a->n_branches, a->window, a->conf, a->argmax, a->dev_status,
+                     lmh_workspace, lmh_workspace_bytes, stream);
+  if (st != LOPA_OK) return st;
+  return launch_step_decide(a, static_cast<cudaStream_t>(stream));
 }

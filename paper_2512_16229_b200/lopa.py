@@ -90,7 +90,9 @@ _SIGS = {
                                  _c_void_p, _c_void_p]),
     "lopa_lmhead_workspace_bytes": (_size, [_i32]),
     "lopa_lmhead_confidence": (_i32, [_c_void_p, _i64, _c_void_p, _i64, _i32, _i32, _i32, _c_void_p,
-                                      _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+                                      _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "lopa_step_lmhead": (_i32, [ctypes.POINTER(StepArgs), _c_void_p, _i64, _c_void_p, _i64, _i32,
+                                _c_void_p, _size, _c_void_p]),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -197,8 +199,8 @@ class LMHead:
         self.conf = torch.empty(max_rows, dtype=torch.float32, device=dev)
         self.argmax = torch.empty(max_rows, dtype=torch.int32, device=dev)
 
-    def __call__(self, hidden: torch.Tensor):
-        _need_cuda(hidden)
+    def __call__(self, hidden: torch.Tensor, row_mask: torch.Tensor | None = None):
+        _need_cuda(hidden, row_mask)
         if hidden.dtype != torch.bfloat16 or hidden.dim() != 2 or hidden.stride(1) != 1:
             raise LopaError("hidden must be a 2-D bf16 tensor [rows][K] with unit inner stride")
         rows = hidden.shape[0]
@@ -206,10 +208,26 @@ class LMHead:
             raise LopaError("hidden shape does not match the weight / max_rows")
         _check(lib().lopa_lmhead_confidence(_p(hidden), hidden.stride(0), _p(self.weight),
                                             self.weight.stride(0), rows, self.hidden_dim, self.vocab,
+                                            _p(None if row_mask is None else _u8(row_mask).contiguous()),
                                             _p(self.conf), _p(self.argmax), _p(self.status),
                                             _p(self.ws), self.ws.numel(), _stream(hidden.device)),
                "lopa_lmhead_confidence")
         return self.conf[:rows], self.argmax[:rows], self.status
+
+    def step(self, stepper: "Stepper", hidden: torch.Tensor, n_branches, branch_tokens, branch_mask):
+        """lopa_step from the verify forward's hidden states (bf16 [max_br][W][K] or
+        [max_br*W][K]): fused LM-head a1, then the stepper's a2-a4.  Returns stepper.out."""
+        _need_cuda(hidden, n_branches, branch_tokens, branch_mask)
+        if stepper.vocab != self.vocab:
+            raise LopaError("stepper vocab does not match the LM-head weight")
+        h = hidden.reshape(-1, hidden.shape[-1])
+        if h.dtype != torch.bfloat16 or h.stride(1) != 1 or h.shape[0] != stepper.max_branches * stepper.window:
+            raise LopaError("hidden must be bf16 [max_branches * window][K] with unit inner stride")
+        a = stepper.args(h, n_branches, branch_tokens, branch_mask)
+        _check(lib().lopa_step_lmhead(ctypes.byref(a), _p(h), h.stride(0), _p(self.weight),
+                                      self.weight.stride(0), self.hidden_dim, _p(self.ws),
+                                      self.ws.numel(), _stream(h.device)), "lopa_step_lmhead")
+        return stepper.out
 
 
 # ----------------------------------------------------------------------------- a3

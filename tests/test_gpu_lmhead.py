@@ -93,3 +93,68 @@ def test_lmhead_repeatable(L):
     for _ in range(3):
         c2, a2, _ = head(hd)
         assert torch.equal(c1, c2) and torch.equal(a1, a2)
+
+
+def _oracle_decisions(conf, amax, tok, msk, n, k, tau):
+    """Alg. 1 decisions (a2-a4) from per-row conf / argmax (oracle functions, fp64)."""
+    from oracle import lopa_oracle as O
+    scores = [O.branch_score(conf[j], msk[j]) for j in range(n)]
+    w = O.verify_select(scores)
+    if not msk[w].any():
+        return scores, w, None, None
+    anc = O.anchor_fill(conf[w], amax[w], tok[w], msk[w], tau)
+    sp = O.spawn_branches(conf[w], amax[w], anc.tokens, anc.mask, k)
+    return scores, w, anc, sp
+
+
+@pytest.mark.parametrize("seed,V,K,W,k", [(0, 5000, 128, 32, 7), (1, 20000, 256, 16, 3),
+                                          (2, 3000, 64, 64, 3), (3, 151936, 3584, 32, 7)])
+def test_step_lmhead(L, seed, V, K, W, k):
+    """lopa_step_lmhead (fused LM-head a1 + the step's a2-a4) against the oracle: conf within
+    R27, and every decision exactly the oracle's decision on the GPU's own conf (and on the
+    fp64 conf unless a near-tie within the conf tolerance governs)."""
+    from oracle import lopa_oracle as O
+    rng = np.random.default_rng(seed)
+    nbr = k + 1
+    h, Wt, _ = syngen.lmhead_inputs(seed, nbr * W, K, V)
+    tok = rng.integers(0, V, size=(nbr, W)).astype(np.int32)
+    msk = (rng.random((nbr, W)) < 0.7).astype(np.uint8)
+    msk[:, 0] = 1
+    n = nbr - 1 if seed % 2 else nbr      # also an absent last branch
+    st = L.Stepper(V, W, nbr, k, 0.9, DEV)
+    head = L.LMHead(_dev(Wt))
+    nb = torch.tensor([n], dtype=torch.int32, device=DEV)
+    out = head.step(st, _dev(h), nb, torch.from_numpy(tok).to(DEV), torch.from_numpy(msk).to(DEV))
+    torch.cuda.synchronize()
+    assert int(out.status.item()) == 0
+    g_conf = out.conf.cpu().numpy().astype(np.float64).reshape(-1)[: n * W].reshape(n, W)
+    g_amax = out.argmax.cpu().numpy().reshape(-1)[: n * W].reshape(n, W)
+    sel = [r for r in range(n * W) if msk.reshape(-1)[r]]
+    rc, ra, ok, Lg = LO.lmhead_confidence(h, Wt, sel)
+    E = LO.logit_error_bound(h, Wt, sel)
+    ref_conf = np.full((n, W), np.nan)
+    ref_amax = np.full((n, W), -1)
+    tol = np.zeros((n, W))
+    for i, r in enumerate(sel):
+        ref_conf[r // W, r % W], ref_amax[r // W, r % W] = rc[i], ra[i]
+        tol[r // W, r % W] = rc[i] * np.expm1(2 * E[i]) + 2e-6
+        assert abs(g_conf[r // W, r % W] - rc[i]) <= tol[r // W, r % W]
+        srt = np.sort(Lg[i])[::-1]
+        if srt[0] - srt[1] >= 2 * E[i]:
+            assert g_amax[r // W, r % W] == ra[i]
+    m = msk[:n].astype(bool)
+    gc = np.where(m, g_conf, np.nan)
+    # decisions exactly the oracle's on the GPU's own conf
+    scores, w, anc, sp = _oracle_decisions(gc, g_amax, tok[:n], msk[:n], n, k, 0.9)
+    assert out.scores.cpu().numpy()[:n].tolist() == [float(np.float32(x)) for x in scores]
+    assert int(out.winner.item()) == O.verify_select([float(np.float32(x)) for x in scores])
+    nn = int(out.n_next.item())
+    if sp is not None:
+        assert nn == len(sp.lookahead) + 1
+        assert np.array_equal(out.next_tokens.cpu().numpy()[:nn], sp.tokens)
+        assert np.array_equal(out.next_mask.cpu().numpy()[:nn], sp.mask)
+    # and the fp64 oracle's decisions unless a near-tie within the conf tolerance governs
+    r_scores, r_w, _, _ = _oracle_decisions(ref_conf, ref_amax, tok[:n], msk[:n], n, k, 0.9)
+    srt = sorted(r_scores, reverse=True)
+    if len(srt) < 2 or srt[0] - srt[1] > 2 * tol.max():
+        assert int(out.winner.item()) == r_w
