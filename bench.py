@@ -40,6 +40,10 @@ CONFIGS = {
     "dream-k15": dict(V=151936, W=32, k=15, tau=0.9, name="D2F-Dream verify step V=151936 W=32 k=15 tau=0.9 (configs[2] shape)"),
     "diffucoder": dict(V=151936, W=32, k=10, tau=0.95, name="D2F-DiffuCoder verify step V=151936 W=32 k=10 tau=0.95 (configs[3] shape)"),
 }
+# NEXT-4: the same step from the verify forward's hidden states (fused LM-head a1), Dream-7B
+# output projection K = 3584 (Qwen2.5-7B hidden size; outside the paper), one GPU
+CONFIGS["lmhead-dream"] = dict(V=151936, W=32, k=7, tau=0.9, K=3584,
+                               name="D2F-Dream verify step from hidden states: fused LM head K=3584 V=151936 W=32 k=7 tau=0.9")
 for _k in (1, 3, 7, 15, 31):
     for _w in (16, 32, 64):
         CONFIGS[f"sweep-k{_k}-w{_w}"] = dict(V=151936, W=_w, k=_k, tau=0.9,
@@ -167,6 +171,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if CFG.get("K"):
+        return run_reference_lmhead(args)
     from oracle import lopa_oracle as O
     import syngen
     V, W, k, tau, seed = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["seed"]
@@ -449,6 +455,170 @@ def run_lopa(args):
     return 0
 
 
+def run_lmhead(args):
+    """--config lmhead-dream: lopa_step_lmhead (tcgen05 LM head with the Conf epilogue, then the
+    decision kernel) on synthetic hidden states and a random-init output projection."""
+    from paper_2512_16229_b200 import lopa
+    import ctypes
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != 1:
+        print(json.dumps({"error": "lmhead-dream runs on one GPU (no branch-parallel LM head yet)"}))
+        return 0
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    V, W, k, tau, Kd = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["K"]
+    st, tok, msk, nb, full, bufs, rows_total, _ = build_workload(lopa, dev, V, W, k, tau, CFG["seed"], 1)
+    del full, bufs
+    rows = (k + 1) * W
+    g = torch.Generator(device=dev).manual_seed(CFG["seed"])
+    NW = 2   # two 1.09 GB weight copies, alternated: every step streams its weights from HBM
+    Ws = [(torch.randn(V, Kd, device=dev, generator=g) / Kd ** 0.5).to(torch.bfloat16) for _ in range(NW)]
+    NH = 8
+    Hs = [(torch.randn(rows, Kd, device=dev, generator=g) * 1.5).to(torch.bfloat16) for _ in range(NH)]
+    heads = [lopa.LMHead(w, max_rows=rows) for w in Ws]
+    L = lopa.lib()
+    stream = torch.cuda.current_stream(dev)
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    argv = [st.args(Hs[0], nb, tok, msk) for _ in range(NW)]
+    refs = [ctypes.byref(a) for a in argv]
+    P_ = lopa._p
+
+    def launch(i):
+        hd = heads[i % NW]
+        s_ = L.lopa_step_lmhead(refs[i % NW], P_(Hs[i % NH]), Kd, P_(hd.weight), Kd, Kd,
+                                P_(hd.ws), hd.ws.numel(), sptr)
+        if s_:
+            raise lopa.LopaError(f"lopa_step_lmhead status {s_}")
+
+    for i in range(args.warmup):
+        launch(i)
+    torch.cuda.synchronize()
+    K = args.steps
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        head_start(stream)
+        t0.record(stream)
+        for i in range(K):
+            launch(i)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    el_ms = t0.elapsed_time(t1)
+    if int(st.out.status.item()) != 0:
+        raise lopa.LopaError(f"device status {int(st.out.status.item())}")
+    # roofline: the LM-head kernel (+ its fold) chained back to back, CUDA events at the ends
+    for i in range(3):
+        heads[i % NW](Hs[i % NH])
+    torch.cuda.synchronize()
+    head_start(stream)
+    t0.record(stream)
+    for i in range(K):
+        heads[i % NW](Hs[i % NH])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    kern_ms = t0.elapsed_time(t1) / K
+    flops = 2.0 * rows * Kd * V
+    pk = peaks()
+    peak = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1416.0)))
+    achieved = flops / (kern_ms / 1000.0) / 1e12
+    # e2e: hidden states + tables from pinned host memory, results back, inside the timed region
+    hh = Hs[0].cpu().pin_memory()
+    h_tok, h_msk, h_nb = tok.cpu().pin_memory(), msk.cpu().pin_memory(), nb.cpu().pin_memory()
+    d_h = torch.empty_like(Hs[0])
+    d_tok, d_msk, d_nb = torch.empty_like(tok), torch.empty_like(msk), torch.empty_like(nb)
+    o = st.out
+    h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory()
+             for t in (o.winner, o.scores, o.next_tokens, o.next_mask, o.n_next, o.status)]
+    ea = st.args(d_h, d_nb, d_tok, d_msk)
+    K2 = max(3, min(K, 200))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(K2):
+        d_h.copy_(hh, non_blocking=True)
+        d_tok.copy_(h_tok, non_blocking=True)
+        d_msk.copy_(h_msk, non_blocking=True)
+        d_nb.copy_(h_nb, non_blocking=True)
+        hd = heads[i % NW]
+        s_ = L.lopa_step_lmhead(ctypes.byref(ea), P_(d_h), Kd, P_(hd.weight), Kd, Kd, P_(hd.ws),
+                                hd.ws.numel(), sptr)
+        if s_:
+            raise lopa.LopaError(f"lopa_step_lmhead status {s_}")
+        for hbuf, dsrc in zip(h_out, (o.winner, o.scores, o.next_tokens, o.next_mask, o.n_next, o.status)):
+            hbuf.copy_(dsrc, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1)
+    h2d = hh.numel() * 2 + tok.numel() * 4 + msk.numel() + nb.numel() * 4
+    d2h = sum(t.numel() * t.element_size() for t in h_out)
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline_lmhead(Hs[0].view(torch.int16).cpu().numpy().view(np.uint16),
+                                  Ws[0].view(torch.int16).cpu().numpy().view(np.uint16), rows)
+    line = {
+        "metric": METRIC, "value": K / (el_ms / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": K,
+        "warmup": args.warmup, "ms_per_step": el_ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init output projection, Gaussian hidden states; transformer body out of scope)",
+        "config": {"workload": CFG["name"], "rows": rows, "masked_rows": rows_total, "hidden": Kd,
+                   "parallelism": "single",
+                   "l2": f"{NW} rotating weight copies ({NW * V * Kd * 2 / 1e9:.2f} GB >= L2)"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "lopa_lmhead_kernel (tcgen05 LM head + Conf epilogue) + its fold",
+                     "kernel_ms_mean": kern_ms,
+                     "kernel_timing": f"CUDA events around {K} back-to-back LMHead calls (GEMM+epilogue kernel and fold kernel)",
+                     "alg_flops_per_launch": flops,
+                     "weight_stream_gbs": V * Kd * 2 / (kern_ms / 1000.0) / 1e9,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, back to back)"},
+        "clocks": clk.summary(),
+        "gpu_launches": K * 3,
+        "e2e": {"value": K2 / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": K2},
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_lmhead(h16, w16, rows, budget_s=12.0):
+    """The NEXT-4 oracle (fp64 logits of bf16 inputs, Conf) on a bounded row sample, one BLAS
+    thread, scaled to steps/s for `rows` rows (the decisions' cost is negligible next to the
+    projection).  h16 / w16: bf16 bit patterns (uint16) on the host."""
+    from oracle import lmhead_oracle as LO
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        n = 0
+        while n < rows and (time.perf_counter() - t0) < budget_s:
+            LO.lmhead_confidence(h16, w16, [n])
+            n += 1
+        dt = time.perf_counter() - t0
+    return {"value": n / dt / rows, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n} of {rows} rows (fp64 logits over V x K, Conf) in {dt:.1f} s, scaled to one step; NumPy 1 thread"}
+
+
+def run_reference_lmhead(args):
+    """Reference arm for --config lmhead-dream: the fp64 oracle on a bounded row sample."""
+    import syngen
+    V, W, k, Kd = CFG["V"], CFG["W"], CFG["k"], CFG["K"]
+    rows = (k + 1) * W
+    h16, w16, _ = syngen.lmhead_inputs(CFG["seed"], rows, Kd, V)
+    cb = cpu_baseline_lmhead(h16, w16, rows, budget_s=20.0)
+    value = cb["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SYN-LMH seeded hidden states and output projection)",
+            "config": {"workload": CFG["name"], "rows": rows, "hidden": Kd},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -462,8 +632,11 @@ def main():
     CFG.update(V=c["V"], W=c["W"], k=c["k"], tau=c["tau"], name=c["name"])
     if args.warmup < 3:
         args.warmup = 3
+    CFG["K"] = c.get("K")
     if args.impl == "reference":
         return run_reference(args)
+    if CFG["K"]:
+        return run_lmhead(args)
     return run_lopa(args)
 
 
