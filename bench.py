@@ -44,6 +44,10 @@ CONFIGS = {
 # output projection K = 3584 (Qwen2.5-7B hidden size; outside the paper), one GPU
 CONFIGS["lmhead-dream"] = dict(V=151936, W=32, k=7, tau=0.9, K=3584,
                                name="D2F-Dream verify step from hidden states: fused LM head K=3584 V=151936 W=32 k=7 tau=0.9")
+# NEXT-1: D2F multi-block windows (2, 4 and 8 active blocks of 32)
+for _k, _w in ((7, 64), (7, 128), (3, 256), (7, 256)):
+    CONFIGS[f"d2f-k{_k}-w{_w}"] = dict(V=151936, W=_w, k=_k, tau=0.9,
+                                       name=f"D2F multi-block window V=151936 W={_w} k={_k} tau=0.9")
 for _k in (1, 3, 7, 15, 31):
     for _w in (16, 32, 64):
         CONFIGS[f"sweep-k{_k}-w{_w}"] = dict(V=151936, W=_w, k=_k, tau=0.9,

@@ -253,6 +253,20 @@ int lopa_syn_generate(uint64_t seed, int32_t block, int32_t vocab, int64_t ld, i
                       int32_t n_branches, const int32_t* branch_tokens,
                       const uint8_t* branch_mask, int32_t extras, void* out, void* stream);
 
+/* NEXT-3 — Commit-Winner-Cache (Figure 3 phase 2): after a BP step
+ * every rank holds the selected branch id in `winner` (device int32, e.g. args->winner of
+ * lopa_bp_step); this makes the winner's payload (its KV features or any per-branch state of
+ * payload_bytes bytes) available on every rank, without a host synchronisation.
+ *   local_payloads device [b_loc][payload_bytes]: this rank's branches rank*b_loc .. +b_loc-1
+ *   out            device [payload_bytes]: receives the winner's payload on every rank
+ *   payload_bytes  a positive multiple of 16; both pointers 16-byte aligned
+ * Mechanism: the owner contributes the payload, every other rank zeros, and one NCCL sum
+ * all-reduce over 32-bit words reassembles it bit-exactly (integers: x + 0 = x).
+ * Two launches on `stream` (a select kernel, then the all-reduce). */
+int lopa_bp_commit_winner(lopa_bp_t* bp, const int32_t* winner, int32_t b_loc,
+                          const void* local_payloads, size_t payload_bytes, void* out,
+                          void* stream);
+
 /* NEXT-4 — the LM-head projection with Conf fused into its epilogue: the logits
  * never reach HBM.  For each row r of the hidden states (the rows of the verify forward whose
  * position is masked; "parallel verification", P:207 logits reuse):

@@ -61,6 +61,46 @@ extern "C" int lopa_bp_step(lopa_bp_t* bp, const lopa_step_args_t* args, int32_t
   return lopa::launch_bp_finish(args, b_loc, bp->world, records, s);
 }
 
+// NEXT-3 Commit-Winner-Cache (Fig. 3 phase 2): every rank contributes the winner's
+// payload if it owns the winner and zeros otherwise; a sum all-reduce over 32-bit words then
+// leaves the owner's bytes on every rank (x + 0 = x exactly on integers).  The root is device
+// data, so no host synchronisation is needed.
+namespace {
+__global__ void commit_select_kernel(const int32_t* winner, int32_t rank, int32_t b_loc,
+                                     const uint4* local, size_t n16, uint4* out) {
+  const int32_t w = *winner;
+  const int32_t owner = w / b_loc;
+  const uint4* src = local + (size_t)(w - owner * b_loc) * n16;
+  const bool mine = owner == rank;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16;
+       i += (size_t)gridDim.x * blockDim.x)
+    out[i] = mine ? src[i] : make_uint4(0u, 0u, 0u, 0u);
+}
+}  // namespace
+
+extern "C" int lopa_bp_commit_winner(lopa_bp_t* bp, const int32_t* winner, int32_t b_loc,
+                                     const void* local_payloads, size_t payload_bytes, void* out,
+                                     void* stream) {
+  if (!bp || !winner || !local_payloads || !out || b_loc < 1 || payload_bytes == 0 ||
+      payload_bytes % 16 != 0)
+    return LOPA_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(local_payloads) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return LOPA_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t n16 = payload_bytes / 16;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, bp->device);
+  const size_t want = (n16 + 255) / 256;
+  const int grid = (int)(want < (size_t)(4 * sms) ? (want ? want : 1) : (size_t)(4 * sms));
+  commit_select_kernel<<<grid, 256, 0, s>>>(winner, bp->rank, b_loc,
+                                            static_cast<const uint4*>(local_payloads), n16,
+                                            static_cast<uint4*>(out));
+  if (cudaGetLastError() != cudaSuccess) return LOPA_ERR_CUDA;
+  if (ncclAllReduce(out, out, payload_bytes / 4, ncclUint32, ncclSum, bp->comm, s) != ncclSuccess)
+    return LOPA_ERR_NCCL;
+  return LOPA_OK;
+}
+
 extern "C" int lopa_bp_check(lopa_bp_t* bp) {
   if (!bp) return LOPA_ERR_INVALID_ARG;
   ncclResult_t async = ncclSuccess;

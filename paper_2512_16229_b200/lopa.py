@@ -82,6 +82,7 @@ _SIGS = {
     "lopa_bp_create": (_i32, [_c_void_p, _i32, _i32, _i32, ctypes.POINTER(_c_void_p)]),
     "lopa_bp_step": (_i32, [_c_void_p, ctypes.POINTER(StepArgs), _i32, _c_void_p, _c_void_p]),
     "lopa_bp_check": (_i32, [_c_void_p]),
+    "lopa_bp_commit_winner": (_i32, [_c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p, _c_void_p]),
     "lopa_bp_destroy": (None, [_c_void_p]),
     "lopa_debug_timeline": (_i32, [_c_void_p, _i32]),
     "lopa_profile_enable": (_i32, [_i32]),
@@ -455,6 +456,22 @@ class BranchParallel:
         _check(lib().lopa_bp_step(self.h, ctypes.byref(a), self.b_loc, _p(self.records),
                                   _stream(s.device)), "lopa_bp_step")
         return s.out
+
+    def commit_winner(self, local_payloads: torch.Tensor, out: torch.Tensor | None = None,
+                      winner: torch.Tensor | None = None) -> torch.Tensor:
+        """NEXT-3 Commit-Winner-Cache: the selected branch's payload (this rank's
+        [b_loc][bytes] buffer holds its own branches') on every rank, no host sync."""
+        _need_cuda(local_payloads)
+        flat = local_payloads.reshape(self.b_loc, -1)
+        nbytes = flat.shape[1] * flat.element_size()
+        if not flat.is_contiguous():
+            raise LopaError("local_payloads must be contiguous [b_loc][...]")
+        if out is None:
+            out = torch.empty(nbytes, dtype=torch.uint8, device=flat.device)
+        w = self.s.out.winner if winner is None else winner
+        _check(lib().lopa_bp_commit_winner(self.h, _p(w), self.b_loc, _p(flat), nbytes, _p(out),
+                                           _stream(flat.device)), "lopa_bp_commit_winner")
+        return out
 
     def check(self):
         _check(lib().lopa_bp_check(self.h), "lopa_bp_check")

@@ -93,3 +93,40 @@ def test_bp_protocol_gloo(world):
     for p in procs:
         p.join(timeout=60)
     assert all(r is True for r in res), res
+
+
+def _commit_worker(rank, world, port, k, nbytes, q):
+    """NEXT-3 Commit-Winner-Cache protocol (lopa_bp_commit_winner): the owner of the winner
+    (rank w // b_loc, bp_shard's partition) contributes its payload, every other rank zeros, and
+    a sum all-reduce over integers leaves the winner's payload bit-exactly on every rank."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2512_16229_b200.lopa import bp_shard
+    ok = True
+    try:
+        b_loc, lo, hi = bp_shard(k + 1, world, rank)
+        pay = lambda j: torch.from_numpy(np.random.default_rng(1000 + j).integers(0, 2**31, nbytes // 4)).to(torch.int64)
+        local = [pay(j) for j in range(lo, lo + b_loc)]
+        for w in range(k + 1):
+            owner = w // b_loc
+            contrib = local[w - lo].clone() if owner == rank else torch.zeros(nbytes // 4, dtype=torch.int64)
+            dist.all_reduce(contrib, op=dist.ReduceOp.SUM)
+            ok &= bool(torch.equal(contrib, pay(w)))
+            ok &= lo <= w < lo + b_loc if owner == rank else not (lo <= w < hi)
+    finally:
+        dist.destroy_process_group()
+    q.put((rank, ok))
+
+
+@pytest.mark.parametrize("world,k", [(2, 7), (4, 7), (4, 14), (2, 2)])
+def test_commit_winner_protocol(world, k):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_commit_worker, args=(r, world, port, k, 256, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world))

@@ -391,6 +391,29 @@ def test_bp_nccl_single_rank(L):
         bp.close()
 
 
+@pytest.mark.parametrize("nbytes", [16, 4096, 1835008])
+def test_bp_commit_winner_single_rank(L, nbytes):
+    """NEXT-3 Commit-Winner-Cache over the real NCCL path (one rank): the winner's payload
+    (KV-sized for the largest case: 28 layers x 2 x 4 KV heads x 128 x 32 positions x 2 B)
+    arrives bit-exactly, for every possible winner; invalid sizes are rejected."""
+    V, W, k, tau = 64, 8, 3, 0.9
+    st = L.Stepper(V, W, k + 1, k, tau, DEV)
+    bp = L.BranchParallel(st, 0, 1)
+    try:
+        g = torch.Generator(device=DEV).manual_seed(nbytes)
+        pay = torch.randint(0, 256, (bp.b_loc, nbytes), dtype=torch.uint8, device=DEV, generator=g)
+        for w in range(bp.b_loc):
+            win = torch.tensor([w], dtype=torch.int32, device=DEV)
+            out = bp.commit_winner(pay, winner=win)
+            torch.cuda.synchronize()
+            assert torch.equal(out, pay[w])
+        bp.check()
+        with pytest.raises(L.LopaError):
+            bp.commit_winner(torch.zeros((bp.b_loc, 12), dtype=torch.uint8, device=DEV))
+    finally:
+        bp.close()
+
+
 # ----------------------------------------------------------------------------- errors
 def test_invalid_args_raise(L):
     t = torch.zeros((2, 60), dtype=torch.bfloat16, device=DEV)
