@@ -57,6 +57,27 @@ if os.path.exists(rep):
                 traffic = None
     out.append("")
     out.append("Units row: " + ", ".join(f"{w}={rr[1][h.index(w)]}" for w in want if w in h))
+rep2 = os.path.join(go, "prof_lmh.ncu-rep")
+if os.path.exists(rep2):
+    raw = subprocess.run(["ncu", "-i", rep2, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    h = rr[0]
+    want = ["gpu__time_duration.sum", "sm__cycles_active.avg", "dram__bytes_read.sum",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+            "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+            "lts__t_sector_hit_rate.pct", "launch__grid_size", "launch__block_size",
+            "launch__registers_per_thread"]
+    want = [w for w in want if w in h]
+    out.append("\n## NEXT-4 fused LM head (`lopa_lmhead_kernel`, --set full, one launch; "
+               "`scripts/lmhead_bench.py`, 241 rows x K=3584 x V=151936)\n")
+    out.append("| kernel | " + " | ".join(want) + " |")
+    out.append("|---|" + "---|" * len(want))
+    for r in rr[2:]:
+        d = dict(zip(h, r))
+        out.append(f"| {d.get('Kernel Name', '')[:24]} | " + " | ".join(d.get(w, "") for w in want) + " |")
+    out.append("")
+    out.append("Units row: " + ", ".join(f"{w}={rr[1][h.index(w)]}" for w in want))
 if traffic:
     json.dump({"bytes_per_launch": traffic, "kernel": "lopa_reduce_kernel", "source": f"profiles/{tag}_ncu_summary.md"},
               open(os.path.join(pr, "traffic.json"), "w"))
