@@ -49,6 +49,16 @@ __device__ __forceinline__ void tl_max(int slot) {
 }
 #define TLMAX(slot) tl_max(slot)
 __device__ __forceinline__ void tl_clk(int slot) { g_timeline[blockIdx.x * kTlSlots + slot] = clock64(); }
+// clock64 read issued only once `dep` is available: the store waits for it (scoreboard) and
+// the clock read follows in program order
+__device__ __forceinline__ void tl_clk_dep(int slot, float dep) {
+  asm volatile("st.global.u32 [%0], %1;" ::"l"(&g_timeline[blockIdx.x * kTlSlots + slot]),
+               "r"(__float_as_uint(dep))
+               : "memory");
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+  g_timeline[blockIdx.x * kTlSlots + slot] = (unsigned long long)t;
+}
 
 #define TLC(slot) tl_clk(slot)
 #else
@@ -169,7 +179,7 @@ __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.w
 __device__ __forceinline__ void touch_global(const void* p) {
   uint32_t d;
   asm volatile("ld.global.cg.u8 %0, [%1];" : "=r"(d) : "l"(p) : "memory");
-  (void)d;
+  asm volatile("" ::"r"(d));
 }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
 
@@ -790,7 +800,11 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
 #define LOPA_TAIL_THREADS 512
 #endif
 constexpr int kTailThreads = LOPA_TAIL_THREADS;
-constexpr size_t kTailSmemBytes = kTailBytes + LOPA_MAX_ROWS * 2;
+// K1's group partials are pulled into K2's shared memory with ONE bulk copy when they fit
+// (the Dream step: 10 groups x 256 rows x 16 B = 41 KB): a single L2 round trip instead of
+// ten loads per thread.
+constexpr size_t kGpStageBytes = 64 * 1024;
+constexpr size_t kTailSmemBytes = kTailBytes + LOPA_MAX_ROWS * 2 + 16 + kGpStageBytes;
 
 
 // Fold one row's group partials (read straight from the group-major workspace: group g of row r
@@ -807,11 +821,30 @@ __device__ __forceinline__ FoldAcc fold_row_global(const float4* q, int n_grp, s
   return fold_seq(n_grp, [&](int p) { return __ldcg(q + p * stride); });
 }
 
+// The same fold with the partials staged in shared memory (group g of row r at q[g * stride]).
+__device__ __forceinline__ FoldAcc fold_row_smem(const float4* q, int n_grp, int stride) {
+  if (n_grp <= 16) {
+    float4 qr[16];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) qr[p] = p < n_grp ? q[p * stride] : make_float4(0.f, 0.f, 0.f, 0.f);
+    return fold_tree16(n_grp, qr);
+  }
+  return fold_seq(n_grp, [&](int p) { return q[p * stride]; });
+}
+
 template <int MODE, int S>
 __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params P) {
   extern __shared__ __align__(128) uint8_t tsm[];
   TailSmem& T = *reinterpret_cast<TailSmem*>(tsm);
   uint16_t* rows = reinterpret_cast<uint16_t*>(tsm + kTailBytes);  // masked rows, ascending
+  uint64_t* gbar = reinterpret_cast<uint64_t*>(tsm + kTailBytes + LOPA_MAX_ROWS * 2);
+  float4* gst = reinterpret_cast<float4*>(tsm + kTailBytes + LOPA_MAX_ROWS * 2 + 16);
+  const size_t gbytes = (size_t)P.n_grp * P.n_cand * sizeof(float4);
+  const bool staged = MODE != MODE_DECIDE && gbytes <= kGpStageBytes;
+  if (threadIdx.x == 0 && staged) {
+    mbar_init(gbar, 1);
+    fence_mbar_init();
+  }
   __shared__ uint32_t s_wcnt[kTailThreads / 32 + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
@@ -895,18 +928,30 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
       T.conf[row] = __ldcg(P.conf + row);
       T.amax[row] = __ldcg(P.argmax + row);
     }
+  } else if (staged) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(gbar, (uint32_t)gbytes);
+      bulk_g2s(gst, P.gpart, (uint32_t)gbytes, gbar, policy_evict_first());
+    }
+    mbar_wait(gbar, 0);
+    if (tid == 0) TLC(23);
+    for (int rc = tid; rc < n_masked; rc += kTailThreads) {
+      const int row = rows[rc];
+      const FoldAcc f = fold_row_smem(gst + row, n_grp, P.n_cand);
+#ifdef LOPA_TIMELINE
+      if (rc == 0) tl_clk_dep(17, f.S);
+#endif
+      const float c = __fdiv_rn(1.0f, f.S);
+      P.conf[row] = c;
+      P.argmax[row] = (int32_t)f.a;
+      if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
+      T.conf[row] = c;
+      T.amax[row] = (int32_t)f.a;
+    }
   } else
   for (int rc = tid; rc < n_masked; rc += kTailThreads) {
     const int row = rows[rc];
     const FoldAcc f = fold_row_global(P.gpart + row, n_grp, (size_t)P.n_cand);
-    if (rc == 0) TLC(17);
-#ifdef LOPA_TIMELINE
-    if (rc == 0) {  // the same loads again (now certainly L2-resident): their latency alone
-      const FoldAcc f2 = fold_row_global(P.gpart + row, n_grp, (size_t)P.n_cand);
-      if (f2.S == 12345.f) P.conf[row] = 0.f;
-      TLC(21);
-    }
-#endif
     const float c = __fdiv_rn(1.0f, f.S);
     P.conf[row] = c;
     P.argmax[row] = (int32_t)f.a;
