@@ -377,6 +377,28 @@ def run_lopa(args):
     pk = peaks()
     peak = float(pk.get("hbm_gbs", 6650.0))
 
+    # Alg. 1 loop captured in one CUDA graph (lopa.StepLoopGraph): 32 iterations whose tables
+    # feed back on the device, replayed; per-iteration time of the captured loop
+    graph_loop = None
+    if world == 1:
+        g_tok, g_msk, g_nb = tok.clone(), msk.clone(), nb.clone()
+        st_g = lopa.Stepper(V, W, k + 1, k, tau, dev)
+        GL = 32
+        gl = lopa.StepLoopGraph(st_g, bufs, g_nb, g_tok, g_msk, GL)
+        reps = 20
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gl.replay()
+        torch.cuda.synchronize()
+        g0.record(stream)
+        for _ in range(reps):
+            g_tok.copy_(tok), g_msk.copy_(msk), g_nb.copy_(nb)
+            gl.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        graph_loop = {"us_per_iteration": g0.elapsed_time(g1) * 1000.0 / (reps * GL), "iterations": GL,
+                      "replays": reps, "note": "one CUDA graph per 32-iteration loop (tables fed back on "
+                      "the device; fixed logits buffers, so later iterations have fewer masked rows)"}
+
     # e2e through the public API with HOST buffers: pinned logits -> device, step, results -> host
     e2e = None
     if world == 1:
@@ -449,6 +471,8 @@ def run_lopa(args):
         }
         if e2e is not None:
             line["e2e"] = e2e
+        if graph_loop is not None:
+            line["graph_loop"] = graph_loop
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

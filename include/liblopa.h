@@ -160,7 +160,9 @@ typedef struct {
   int32_t vocab;
   int32_t window;                /* W <= LOPA_MAX_WINDOW                                      */
   int32_t max_branches;          /* table capacity (k + 1 for a steady-state loop)           */
-  const int32_t* n_branches;     /* device scalar: branches present in the tables / logits   */
+  const int32_t* n_branches;     /* device scalar: branches present in the tables / logits;
+                                    0 (a complete block fed back, R21): row 0 passes through,
+                                    n_branches_next = 0                                         */
   const int32_t* branch_tokens;  /* device int32 [max_branches][window]                      */
   const uint8_t* branch_mask;    /* device uint8 [max_branches][window]                      */
   int32_t k;                     /* lookahead budget for the next spawn, k + 1 <= LOPA_MAX_BRANCHES */

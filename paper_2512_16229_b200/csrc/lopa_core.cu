@@ -488,6 +488,20 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
   const int warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
   const int nb = max(0, min(*P.n_branches, P.cap));
+  if (nb == 0) {  // no branch (the block was already complete, R21): pass row 0 through
+    if (tid < W) {
+      P.next_tokens[tid] = P.branch_tokens[tid];
+      P.next_mask[tid] = P.branch_mask[tid];
+    }
+    if (P.lookahead)
+      for (int q = tid; q < P.k; q += NT) P.lookahead[q] = -1;
+    for (int j = tid; j < P.cap; j += NT) P.scores[j] = -INFINITY;
+    if (tid == 0) {
+      *P.winner = 0;
+      *P.n_next = 0;
+    }
+    return;
+  }
   cta_scores<NT, S>(T, P, nb, W, warp, lane, P.scores);
   __syncthreads();
   if (tid == 0) TLC(22);
@@ -1173,6 +1187,14 @@ static int ensure_kernel_attrs(int device) {
 
 bool bind_device(void* stream, const void* ptr, int* device) {
   int dev = -1;
+  if (stream != nullptr) {
+    // During CUDA-graph capture, device queries on the stream invalidate the capture: the
+    // capturing thread's current device is the stream's device.
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cs) == cudaSuccess &&
+        cs != cudaStreamCaptureStatusNone)
+      return cudaGetDevice(device) == cudaSuccess;
+  }
   if (stream != nullptr) {
     if (cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &dev) != cudaSuccess) dev = -1;
   }

@@ -364,6 +364,45 @@ class Stepper:
         return self.out
 
 
+class StepLoopGraph:
+    """`iters` Alg. 1 iterations captured in ONE CUDA graph (no tracing compiler, no host
+    round trip between steps): each iteration is a lopa_step on logits[i % len(logits)]
+    followed by a device copy of the spawned tables into the step's input tables.  The logits
+    buffers are the caller's (a model would write them between steps; the graph reads whatever
+    they hold at replay).  replay() runs the whole loop; the stepper's outputs and the input
+    tables then hold the last iteration's state (a complete block rests at its fixed point:
+    n_branches = 0 passes row 0 through)."""
+
+    def __init__(self, stepper: Stepper, logits: list, n_branches, branch_tokens, branch_mask,
+                 iters: int):
+        _need_cuda(n_branches, branch_tokens, branch_mask, *logits)
+        self.s, self.logits, self.iters = stepper, logits, iters
+        self.nb, self.tok, self.msk = n_branches, branch_tokens, _u8(branch_mask)
+        for lg in logits:
+            stepper._validate(lg, n_branches, branch_tokens, self.msk)
+        self._args = [stepper.args(lg, n_branches, branch_tokens, self.msk) for lg in logits]
+        # warm up outside the capture (kernel attributes, lazy module loading)
+        self._iteration(0)
+        torch.cuda.synchronize(stepper.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            for i in range(iters):
+                self._iteration(i)
+
+    def _iteration(self, i):
+        o = self.s.out
+        a = self._args[i % len(self._args)]
+        _check(lib().lopa_step(ctypes.byref(a), _stream(self.s.device)), "lopa_step")
+        k1 = o.next_tokens.shape[0]
+        self.tok[:k1].copy_(o.next_tokens)
+        self.msk[:k1].copy_(o.next_mask)
+        self.nb.copy_(o.n_next)
+
+    def replay(self):
+        self.graph.replay()
+        return self.s.out
+
+
 # ----------------------------------------------------------------------------- measurement
 def profile_enable(max_records: int):
     """Record CUDA events around every K1 (vocabulary reduction) launch of the next calls."""

@@ -592,3 +592,58 @@ def test_step_wide_windows(L, V, W, k):
         if int(out.n_next.item()) == 0:
             break
         tok, msk, nb = out.next_tokens.clone(), out.next_mask.clone(), out.n_next.clone()
+
+
+# ----------------------------------------------------------------------------- CUDA graph loop
+def test_step_loop_graph_matches_eager(L):
+    """A 10-iteration Alg. 1 loop captured in one CUDA graph (lopa.StepLoopGraph) visits the
+    same states as the same loop run eagerly step by step (fixed logits buffers per iteration;
+    the tables feed back on the device)."""
+    V, W, k, tau = 1000, 32, 5, 0.9
+    g = torch.Generator(device=DEV).manual_seed(3)
+    bufs = [(torch.randn((k + 1, W, 1000), generator=g, device=DEV) * 3).to(torch.bfloat16) for _ in range(3)]
+
+    def fresh():
+        tok, msk, nb = G.fresh_tables(k, W, DEV)
+        return tok, msk, nb
+
+    st_e = L.Stepper(V, W, k + 1, k, tau, DEV)
+    tok, msk, nb = fresh()
+    trace_e = []
+    for i in range(10):
+        o = st_e.step(bufs[i % 3], nb, tok, msk)
+        trace_e.append((int(o.winner.item()), int(o.n_next.item())))
+        tok[: k + 1].copy_(o.next_tokens)
+        msk[: k + 1].copy_(o.next_mask)
+        nb.copy_(o.n_next)
+    final_e = (tok.clone(), msk.clone())
+    st_g = L.Stepper(V, W, k + 1, k, tau, DEV)
+    tok, msk, nb = fresh()
+    t0, m0 = tok.clone(), msk.clone()
+    gl = L.StepLoopGraph(st_g, bufs, nb, tok, msk, 10)
+    # the constructor ran one warm-up iteration: restore the initial state, then replay
+    tok.copy_(t0), msk.copy_(m0), nb.fill_(1)
+    gl.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(tok, final_e[0]) and torch.equal(msk, final_e[1])
+    assert (int(st_g.out.winner.item()), int(st_g.out.n_next.item())) == trace_e[-1]
+    # replaying again from the same start gives the same result (the graph is reusable)
+    tok.copy_(t0), msk.copy_(m0), nb.fill_(1)
+    gl.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(tok, final_e[0]) and torch.equal(msk, final_e[1])
+
+
+def test_step_without_branches_passes_through(L):
+    """n_branches = 0 (a complete block fed back into the step, R21): row 0 passes through,
+    n_branches_next = 0, winner 0 — so a graph-captured loop rests at its fixed point."""
+    V, W, k = 64, 8, 2
+    st = L.Stepper(V, W, k + 1, k, 0.9, DEV)
+    tok = torch.arange((k + 1) * W, dtype=torch.int32, device=DEV).reshape(k + 1, W)
+    msk = torch.zeros((k + 1, W), dtype=torch.uint8, device=DEV)
+    nb = torch.zeros(1, dtype=torch.int32, device=DEV)
+    logits = torch.zeros((k + 1, W, st.ld), dtype=torch.bfloat16, device=DEV)
+    o = st.step(logits, nb, tok, msk)
+    torch.cuda.synchronize()
+    assert int(o.n_next.item()) == 0 and int(o.winner.item()) == 0 and int(o.status.item()) == 0
+    assert torch.equal(o.next_tokens[0], tok[0]) and torch.equal(o.next_mask[0], msk[0])
