@@ -252,18 +252,21 @@ def run_lopa(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     V, W, k, tau, seed, n_buf = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["seed"], CFG["n_buf"]
-    if world > 1:
+    # LOPA_BENCH_FORCE_BP=1 runs the branch-parallel path (NCCL communicator of one rank) at N=1,
+    # to exercise the N > 1 code path on a single GPU
+    use_bp = world > 1 or os.environ.get("LOPA_BENCH_FORCE_BP") == "1"
+    if use_bp:
         b_loc, lo, hi = lopa.bp_shard(k + 1, world, rank)
     else:
         b_loc, lo, hi = k + 1, 0, k + 1
     st, tok, msk, nb, full, bufs, rows_total, rows_local = build_workload(
-        lopa, dev, V, W, k, tau, seed, n_buf, lo, hi, b_loc if world > 1 else None)
+        lopa, dev, V, W, k, tau, seed, n_buf, lo, hi, b_loc if use_bp else None)
     stream = torch.cuda.current_stream(dev)
     sptr = ctypes.c_void_p(stream.cuda_stream)
     L = lopa.lib()
 
     bp = None
-    if world > 1:
+    if use_bp:
         bp = lopa.BranchParallel(st, rank, world)
 
     # prebuilt argument structs (one per rotating buffer): the timed loop only launches
@@ -380,7 +383,7 @@ def run_lopa(args):
     # Alg. 1 loop captured in one CUDA graph (lopa.StepLoopGraph): 32 iterations whose tables
     # feed back on the device, replayed; per-iteration time of the captured loop
     graph_loop = None
-    if world == 1:
+    if world == 1 and bp is None:
         g_tok, g_msk, g_nb = tok.clone(), msk.clone(), nb.clone()
         st_g = lopa.Stepper(V, W, k + 1, k, tau, dev)
         GL = 32
@@ -454,7 +457,7 @@ def run_lopa(args):
             "config": {"workload": CFG.get("name", "D2F-Dream verify step V=151936 W=32 k=7 tau=0.9 (configs[1])"),
                        "branches": int(nb.item()), "masked_rows": rows_total,
                        "masked_rows_this_rank": rows_local,
-                       "parallelism": f"bp{world}" if world > 1 else "single",
+                       "parallelism": f"bp{world}" if bp is not None else "single",
                        "l2": f"rotating {n_buf} logits buffers ({n_buf * full.numel() * 2 / 1e6:.0f} MB >= 4x L2)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -467,7 +470,7 @@ def run_lopa(args):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "_fallback" not in pk else "fallback"},
             "logits_gbs_step": alg_bytes / (el_ms / K / 1000.0) / 1e9,
             "clocks": clk.summary(),
-            "gpu_launches": K * (2 if world == 1 else 3),
+            "gpu_launches": K * (2 if bp is None else 3),
         }
         if e2e is not None:
             line["e2e"] = e2e
