@@ -111,12 +111,15 @@ class BlockPipeline:
 
 def decode_d2f(forward_block, gen_len: int, k: int, cfg: BlockConfig, vocab: int, device,
                tokens0: torch.Tensor | None = None, max_forwards: int | None = None,
-               metric: int = lopa.METRIC_MEAN, metric_param: float = 0.0) -> D2FResult:
+               metric: int = lopa.METRIC_MEAN, metric_param: float = 0.0,
+               on_step=None) -> D2FResult:
     """LoPA decoding of a ``gen_len``-token region through the D2F block pipeline.
 
     ``forward_block(b, tokens[n][B], mask[n][B]) -> bf16 [n][B][ld]`` is the model stand-in for
     the positions of block b under n branch states (device tensors); a window forward is one
-    call per active block, placed side by side in the window's logits buffer."""
+    call per active block, placed side by side in the window's logits buffer.
+    ``on_step(iteration, logits, branch_tokens, branch_mask, n, thresholds, outputs)`` (optional,
+    for tests and tracing) sees every step's inputs and outputs right after the step."""
     B = cfg.block_size
     if gen_len % B:
         raise lopa.LopaError("gen_len must be a multiple of block_size")
@@ -148,6 +151,8 @@ def decode_d2f(forward_block, gen_len: int, k: int, cfg: BlockConfig, vocab: int
                                                            br_msk[:n, c * B:(c + 1) * B].contiguous())
         nb_dev.fill_(n)
         out = st.step(logits, nb_dev, br_tok, br_msk)
+        if on_step is not None:
+            on_step(res.forwards, logits, br_tok, br_msk, n, pipe.thresholds(), out)
         res.forwards += 1
         res.windows.append((p0, W))
         res.branch_counts.append(n)
