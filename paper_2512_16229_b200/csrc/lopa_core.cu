@@ -857,6 +857,15 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
     mbar_init(gbar, 1);
     fence_mbar_init();
   }
+  // When 16 group slots of every row fit, the slots past n_grp hold neutral partials
+  // (m = -inf, s = 0), so the 16-slot fold runs without predicates (identical bits: a neutral
+  // slot adds +0 and never matches the maximum).
+  const bool staged16 = staged && P.n_grp <= 16 && (size_t)P.n_cand * 16 * sizeof(float4) <= kGpStageBytes;
+  if (staged16) {
+    const float4 neutral = make_float4(-INFINITY, 0.f, __uint_as_float(0xFFFFFFFFu), 0.f);
+    for (int e = threadIdx.x; e < (16 - P.n_grp) * P.n_cand; e += kTailThreads)
+      gst[(size_t)P.n_grp * P.n_cand + e] = neutral;
+  }
   __shared__ uint32_t s_wcnt[kTailThreads / 32 + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
@@ -947,13 +956,39 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
     }
     mbar_wait(gbar, 0);
     if (tid == 0) TLC(23);
+    const int stride = P.n_cand;
     for (int rc = tid; rc < n_masked; rc += kTailThreads) {
       const int row = rows[rc];
+      if (staged16) {
+        float4 qr[16];
+#pragma unroll
+        for (int p = 0; p < 16; ++p) qr[p] = gst[row + p * stride];
+        const FoldAcc f = fold_tree16(16, qr);
+#ifdef LOPA_TIMELINE
+        if (rc == 0) tl_clk_dep(17, f.S);
+#endif
+        const float c = __fdiv_rn(1.0f, f.S);
+        P.conf[row] = c;
+        P.argmax[row] = (int32_t)f.a;
+        if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
+        T.conf[row] = c;
+        T.amax[row] = (int32_t)f.a;
+        continue;
+      }
+#ifdef LOPA_TIMELINE
+      if (rc == 0) {
+        const float4 q0 = gst[row];
+        tl_clk_dep(21, q0.x);  // one staged partial read back
+      }
+#endif
       const FoldAcc f = fold_row_smem(gst + row, n_grp, P.n_cand);
 #ifdef LOPA_TIMELINE
       if (rc == 0) tl_clk_dep(17, f.S);
 #endif
       const float c = __fdiv_rn(1.0f, f.S);
+#ifdef LOPA_TIMELINE
+      if (rc == 0) tl_clk_dep(22, c);
+#endif
       P.conf[row] = c;
       P.argmax[row] = (int32_t)f.a;
       if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);

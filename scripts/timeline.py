@@ -25,7 +25,7 @@ for rep in range(int(os.environ.get('REPS', 3))):
              "k2_start", "k2_folded", "gp_loaded", "anchored", "gp_bar", "rows_folded", "sp_rank", "sp_write", "prod_done", "fold_bar"]
     c = a[0]
     print(f"rep {rep}: rows={rows} k2 clocks after wait: row0 folded {c[17]-c[16]}, loop end {c[18]-c[16]}, "
-          f"first partial loaded {c[23]-c[16]}, fold barrier {c[19]-c[16]}, scores barrier {c[22]-c[16]}, end {c[20]-c[16]}")
+          f"partials staged {c[23]-c[16]}, one read {c[21]-c[16]}, row0 divided {c[22]-c[16]}, fold barrier {c[19]-c[16]}, scores barrier {c[22]-c[16]}, end {c[20]-c[16]}")
     for j, nm in enumerate(names):
         col = rel[:, j]
         col = col[(a[:, j] > 0) & (a[:, j] >= t0)]
