@@ -484,10 +484,10 @@ __device__ __forceinline__ void cta_scores(TailSmem& T, const Params& P, int nb,
 // a2 -> a3 -> a4 with the tail CTA (T.conf / T.amax hold the folded rows).  After the scores,
 // warps 0..S-1 (32 S threads = one per window position) finish with a named barrier.
 template <int NT, int S>
-__device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
+__device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
+  // nb = branches present, read by the kernel's prologue (no global load on the tail's path)
   const int warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
-  const int nb = max(0, min(*P.n_branches, P.cap));
   if (nb == 0) {  // no branch (the block was already complete, R21): pass row 0 through
     if (tid < W) {
       P.next_tokens[tid] = P.branch_tokens[tid];
@@ -590,10 +590,9 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid) {
 // Local half of a BP step with all threads of the last CTA: local Eq. 2 scores, local best
 // (smallest local j with the largest score), and the exchange record.
 template <int NT, int S>
-__device__ void cta_tail_bp_local(const Params& P, TailSmem& T, int tid) {
+__device__ void cta_tail_bp_local(const Params& P, TailSmem& T, int tid, int nb) {
   const int warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
-  const int nb = max(0, min(*P.n_branches - P.branch_base, P.cap));
   RecordView rv = record_view(P.record, P.cap);
   cta_scores<NT, S>(T, P, nb, W, warp, lane, rv.scores);
   __syncthreads();
@@ -1009,8 +1008,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   if (tid == 0) TLC(18);
   __syncthreads();
   if (tid == 0) { TL(7); TLC(19); }
-  if (MODE == MODE_STEP || MODE == MODE_DECIDE) cta_tail_step<kTailThreads, S>(P, T, tid);
-  if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads, S>(P, T, tid);
+  if (MODE == MODE_STEP || MODE == MODE_DECIDE) cta_tail_step<kTailThreads, S>(P, T, tid, nb);
+  if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads, S>(P, T, tid, nb);
   if (tid == 0) {
     P.ctrs[0] = 0;
     TL(5);
