@@ -455,6 +455,7 @@ struct TailSmem {
   int32_t b0_amax[LOPA_MAX_WINDOW];
   uint8_t b0_msk[LOPA_MAX_WINDOW];
   int32_t rank[LOPA_MAX_WINDOW];
+  float taus[LOPA_MAX_WINDOW];  // per-position thresholds (staged from P.tau_pos, if any)
   int32_t n;       // lookahead count, -1 = winner complete
   int32_t best;    // (BP) local best
   double dscr[kScoreWarps][LOPA_MAX_WINDOW];  // per-warp metric scratch
@@ -525,7 +526,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
 #pragma unroll
     for (int h = 0; h < S; ++h) anym |= r.msk[h] != 0;
     const bool any = __any_sync(0xffffffffu, anym);
-    if (any) warp_anchor<S>(r, P.tau, P.tau_pos, W, lane);
+    if (any) warp_anchor<S>(r, P.tau, P.tau_pos ? T.taus : nullptr, W, lane);
     int n_mb0 = 0;
 #pragma unroll
     for (int h = 0; h < S; ++h) {
@@ -891,6 +892,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
     mine[u] = mk ? 1u : 0u;
     cnt += mk ? 1 : 0;
   }
+  if (P.tau_pos)
+    for (int i = tid; i < W; i += kTailThreads) T.taus[i] = P.tau_pos[i];
   // block-wide exclusive scan of the per-thread masked counts -> compacted row list
   int incl = cnt;
 #pragma unroll
@@ -1182,6 +1185,17 @@ int num_sms(int device) {
   return g_sms[device];
 }
 
+// The K2 instantiation for a mode and window: S = window slots per lane (1, 2 or 8).
+using TailKernel = void (*)(const Params);
+static TailKernel tail_kernel_for(int mode, int window) {
+  const int S = window <= 32 ? 1 : (window <= 64 ? 2 : 8);
+  if (mode == MODE_STEP)
+    return S == 1 ? lopa_tail_kernel<MODE_STEP, 1> : S == 2 ? lopa_tail_kernel<MODE_STEP, 2> : lopa_tail_kernel<MODE_STEP, 8>;
+  if (mode == MODE_DECIDE)
+    return S == 1 ? lopa_tail_kernel<MODE_DECIDE, 1> : S == 2 ? lopa_tail_kernel<MODE_DECIDE, 2> : lopa_tail_kernel<MODE_DECIDE, 8>;
+  return S == 1 ? lopa_tail_kernel<MODE_BP_LOCAL, 1> : S == 2 ? lopa_tail_kernel<MODE_BP_LOCAL, 2> : lopa_tail_kernel<MODE_BP_LOCAL, 8>;
+}
+
 static int ensure_kernel_attrs(int device) {
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -1193,25 +1207,13 @@ static int ensure_kernel_attrs(int device) {
     return LOPA_ERR_CUDA;
   if (major != 10 || minor != 0) return LOPA_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(lopa_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kSmemBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(lopa_tail_kernel<MODE_STEP, 2>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(lopa_tail_kernel<MODE_STEP, 8>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(lopa_tail_kernel<MODE_BP_LOCAL, 2>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(lopa_tail_kernel<MODE_BP_LOCAL, 8>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(lopa_tail_kernel<MODE_DECIDE, 2>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(lopa_tail_kernel<MODE_DECIDE, 8>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmemBytes) != cudaSuccess)
+                           (int)kSmemBytes) != cudaSuccess)
     return LOPA_ERR_CUDA;
-#ifdef LOPA_CARVEOUT
-  cudaFuncSetAttribute(lopa_reduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, LOPA_CARVEOUT);
-  cudaFuncSetAttribute(lopa_tail_kernel<MODE_STEP, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, LOPA_CARVEOUT);
-  cudaFuncSetAttribute(lopa_tail_kernel<MODE_STEP, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, LOPA_CARVEOUT);
-#endif
+  for (int mode : {(int)MODE_STEP, (int)MODE_BP_LOCAL, (int)MODE_DECIDE})
+    for (int w : {32, 64, 256})
+      if (cudaFuncSetAttribute(tail_kernel_for(mode, w), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kTailSmemBytes) != cudaSuccess)
+        return LOPA_ERR_CUDA;
   std::lock_guard<std::mutex> lk(g_mu);
   if (device >= 0 && device < 64) g_attr[device] = true;
   return LOPA_OK;
@@ -1319,10 +1321,8 @@ static int launch_reduce(const Params& P, int device, cudaStream_t s) {
     e = launch_pdl(lopa_fold_kernel, dim3(nb), dim3(256), 0, s, P);
   } else {
     // window slots per lane: 2 (W <= 64) or 8 (the D2F multi-block window, W <= 256)
-    const bool wide = P.window > 64;
-    auto kern = P.mode == MODE_STEP ? (wide ? lopa_tail_kernel<MODE_STEP, 8> : lopa_tail_kernel<MODE_STEP, 2>)
-                                    : (wide ? lopa_tail_kernel<MODE_BP_LOCAL, 8>
-                                            : lopa_tail_kernel<MODE_BP_LOCAL, 2>);
+    // window slots per lane: 1 (W <= 32), 2 (W <= 64), 8 (the D2F multi-block window)
+    auto kern = tail_kernel_for(P.mode, P.window);
     e = launch_pdl(kern, dim3(1), dim3(kTailThreads), kTailSmemBytes, s, P);
   }
   return cuda_status(e);
@@ -1432,7 +1432,7 @@ int launch_step_decide(const lopa_step_args_t* a, cudaStream_t s) {
   P.cap = a->max_branches;
   P.n_cand = rows;
   P.row_mask = a->branch_mask;
-  auto kern = P.window > 64 ? lopa_tail_kernel<MODE_DECIDE, 8> : lopa_tail_kernel<MODE_DECIDE, 2>;
+  auto kern = tail_kernel_for(MODE_DECIDE, P.window);
   return cuda_status(launch_pdl(kern, dim3(1), dim3(kTailThreads), kTailSmemBytes, s, P));
 }
 
