@@ -431,13 +431,16 @@ __device__ __forceinline__ FoldAcc fold_tree16(int n, const float4 (&q)[16]) {
   uint32_t a = 0xFFFFFFFFu;
 #pragma unroll
   for (int p = 0; p < 16; ++p) {
-    t[p] = p < n ? q[p].y * (M == -INFINITY ? 1.f : ex2((q[p].x - M) * kLog2e)) : 0.f;
+    // explicit _rn operations: no FMA contraction, so every instantiation (runtime or
+    // compile-time n) rounds identically
+    t[p] = p < n ? __fmul_rn(q[p].y, M == -INFINITY ? 1.f : ex2(__fmul_rn(__fsub_rn(q[p].x, M), kLog2e)))
+                 : 0.f;
     a = (p < n && q[p].x == M) ? min(a, __float_as_uint(q[p].z)) : a;
   }
 #pragma unroll
   for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
-    for (int p = 0; p < w; ++p) t[p] = t[2 * p] + t[2 * p + 1];
+    for (int p = 0; p < w; ++p) t[p] = __fadd_rn(t[2 * p], t[2 * p + 1]);
   return FoldAcc{M, t[0], a};
 }
 
