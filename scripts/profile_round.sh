@@ -8,3 +8,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"lopa_(reduce|tail)" -s 8 -c 4 -o gpurun_out/prof_full -f python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?" >> gpurun_out/b20.log
 N=3 NW=1 timeout 300 python scripts/lmhead_bench.py > gpurun_out/lmhb_plain.log 2>&1 && \
 N=3 NW=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:lopa_lmhead_kernel -s 2 -c 1 -o gpurun_out/prof_lmh -f python scripts/lmhead_bench.py > gpurun_out/ncu_lmh.log 2>&1; echo "ncu lmh rc=$?" >> gpurun_out/b20.log
+LOPA_LIB_VARIANT=tl REPS=2 timeout 120 python scripts/timeline.py > gpurun_out/tl.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
