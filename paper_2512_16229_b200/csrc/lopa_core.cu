@@ -1024,13 +1024,50 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
 }
 
 // MODE_CONF: one thread per candidate row, no decisions.
-__global__ void __launch_bounds__(256) lopa_fold_kernel(const Params P) {
+// One block per 256 rows.  With <= 16 groups the block's partials are pulled into shared
+// memory with one bulk copy per group (a single L2 round trip), as in K2; beyond that each
+// thread reads its row's partials directly.
+constexpr int kFoldRows = 256;
+constexpr size_t kFoldSmemBytes = 16 + (size_t)16 * kFoldRows * sizeof(float4);
+__global__ void __launch_bounds__(kFoldRows) lopa_fold_kernel(const Params P) {
+  extern __shared__ __align__(16) uint8_t fsm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fsm);
+  float4* st = reinterpret_cast<float4*>(fsm + 16);  // [16][kFoldRows]
   grid_dep_launch();
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r0 = blockIdx.x * kFoldRows;
+  const int nrows = min(kFoldRows, P.n_cand - r0);
+  const int r = r0 + threadIdx.x;
   const bool valid = r < P.n_cand && (P.row_mask == nullptr || P.row_mask[r] != 0);
+  const bool staged = P.n_grp <= 16;
+  if (staged) {
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+    }
+    const float4 neutral = make_float4(-INFINITY, 0.f, __uint_as_float(0xFFFFFFFFu), 0.f);
+    for (int e = threadIdx.x; e < (16 - P.n_grp) * kFoldRows; e += kFoldRows)
+      st[P.n_grp * kFoldRows + e] = neutral;
+    __syncthreads();
+  }
   grid_dep_wait();
+  FoldAcc f;
+  if (staged) {
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)(nrows * sizeof(float4));
+      mbar_arrive_expect_tx(bar, bytes * (uint32_t)P.n_grp);
+      const uint64_t pol = policy_evict_first();
+      for (int g = 0; g < P.n_grp; ++g)
+        bulk_g2s(st + g * kFoldRows, P.gpart + (size_t)g * P.n_cand + r0, bytes, bar, pol);
+    }
+    mbar_wait(bar, 0);
+    float4 qr[16];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) qr[p] = st[p * kFoldRows + threadIdx.x];
+    f = fold_tree16(16, qr);
+  } else if (valid) {
+    f = fold_row_global(P.gpart + r, P.n_grp, (size_t)P.n_cand);
+  }
   if (valid) {
-    const FoldAcc f = fold_row_global(P.gpart + r, P.n_grp, (size_t)P.n_cand);
     P.conf[r] = __fdiv_rn(1.0f, f.S);
     P.argmax[r] = (int32_t)f.a;
     if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
@@ -1210,7 +1247,9 @@ static int ensure_kernel_attrs(int device) {
     return LOPA_ERR_CUDA;
   if (major != 10 || minor != 0) return LOPA_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(lopa_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kSmemBytes) != cudaSuccess)
+                           (int)kSmemBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(lopa_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kFoldSmemBytes) != cudaSuccess)
     return LOPA_ERR_CUDA;
   for (int mode : {(int)MODE_STEP, (int)MODE_BP_LOCAL, (int)MODE_DECIDE})
     for (int w : {32, 64, 256})
@@ -1321,7 +1360,7 @@ static int launch_reduce(const Params& P, int device, cudaStream_t s) {
   prof_record(1, s, &pslot);
   if (P.mode == MODE_CONF) {
     const int nb = (P.n_cand + 255) / 256;
-    e = launch_pdl(lopa_fold_kernel, dim3(nb), dim3(256), 0, s, P);
+    e = launch_pdl(lopa_fold_kernel, dim3(nb), dim3(kFoldRows), kFoldSmemBytes, s, P);
   } else {
     // window slots per lane: 2 (W <= 64) or 8 (the D2F multi-block window, W <= 256)
     // window slots per lane: 1 (W <= 32), 2 (W <= 64), 8 (the D2F multi-block window)
