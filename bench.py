@@ -267,7 +267,8 @@ def run_lopa(args):
 
     bp = None
     if use_bp:
-        bp = lopa.BranchParallel(st, rank, world)
+        # LOPA_BP_P2P=1: the record exchange over peer memory (lopa_bp_step_p2p) instead of NCCL
+        bp = lopa.BranchParallel(st, rank, world, p2p=os.environ.get("LOPA_BP_P2P") == "1")
 
     # prebuilt argument structs (one per rotating buffer): the timed loop only launches
     if bp is None:
@@ -290,7 +291,10 @@ def run_lopa(args):
         rec = ctypes.c_void_p(bp.records.data_ptr())
 
         def launch(i):
-            s = L.lopa_bp_step(bp.h, refs[i % n_buf], bp.b_loc, rec, sptr)
+            if bp.p2p:
+                s = L.lopa_bp_step_p2p(bp.h, refs[i % n_buf], bp.b_loc, sptr)
+            else:
+                s = L.lopa_bp_step(bp.h, refs[i % n_buf], bp.b_loc, rec, sptr)
             if s:
                 raise lopa.LopaError(f"lopa_bp_step status {s}")
 
@@ -457,7 +461,7 @@ def run_lopa(args):
             "config": {"workload": CFG.get("name", "D2F-Dream verify step V=151936 W=32 k=7 tau=0.9 (configs[1])"),
                        "branches": int(nb.item()), "masked_rows": rows_total,
                        "masked_rows_this_rank": rows_local,
-                       "parallelism": f"bp{world}" if bp is not None else "single",
+                       "parallelism": (f"bp{world}" + ("-p2p" if bp.p2p else "")) if bp is not None else "single",
                        "l2": f"rotating {n_buf} logits buffers ({n_buf * full.numel() * 2 / 1e6:.0f} MB >= 4x L2)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -69,6 +69,8 @@ typedef enum {
 #define LOPA_DEV_EMPTY_MASK 1 /* Eq. 1 applied with nothing masked           */
 #define LOPA_DEV_NONFINITE 2  /* a reduced row holds NaN or +inf, or is all -inf (R20);
                                  that row's conf / argmax are unspecified                   */
+#define LOPA_DEV_PEER_TIMEOUT 4 /* lopa_bp_step_p2p: a peer's record did not arrive (bounded
+                                   wait); that step's decisions are unspecified            */
 
 #define LOPA_MAX_WINDOW 256   /* W <= 256 (the D2F multi-block window); W > 64 needs V <= 2^22 */
 #define LOPA_MAX_BRANCHES 32  /* k + 1 <= 32: one lane per branch in the select             */
@@ -254,6 +256,23 @@ int lopa_debug_timeline(unsigned long long* out, int n_ctas);
 int lopa_syn_generate(uint64_t seed, int32_t block, int32_t vocab, int64_t ld, int32_t window,
                       int32_t n_branches, const int32_t* branch_tokens,
                       const uint8_t* branch_mask, int32_t extras, void* out, void* stream);
+
+/* Branch parallelism over peer memory (the exchange of lopa_bp_step without NCCL): each rank
+ * writes its record straight into every peer's record buffer over NVLink (CUDA IPC mapping)
+ * and raises a per-rank epoch flag there (release at system scope); the finishing kernel
+ * waits for every rank's flag of this step (acquire) and runs the same deterministic select /
+ * anchor / spawn.  Records are double-buffered by epoch parity, so a rank may run one step
+ * ahead of a slow reader.  Same results as lopa_bp_step.
+ *   lopa_bp_p2p_alloc: allocates this rank's buffers for (window <= 256, b_loc) and writes
+ *     its IPC handle (LOPA_BP_IPC_HANDLE_BYTES) to handle_out; call once per communicator.
+ *   lopa_bp_p2p_open: all_handles = the world handles in rank order (gathered by the caller);
+ *     maps every peer's buffers.
+ *   lopa_bp_step_p2p: as lopa_bp_step (args, b_loc), on the P2P buffers.
+ * Errors: LOPA_ERR_INVALID_ARG (order of calls, sizes), LOPA_ERR_CUDA (allocation, IPC). */
+#define LOPA_BP_IPC_HANDLE_BYTES 64
+int lopa_bp_p2p_alloc(lopa_bp_t* bp, int32_t window, int32_t b_loc, void* handle_out);
+int lopa_bp_p2p_open(lopa_bp_t* bp, const void* all_handles);
+int lopa_bp_step_p2p(lopa_bp_t* bp, const lopa_step_args_t* args, int32_t b_loc, void* stream);
 
 /* NEXT-3 — Commit-Winner-Cache (Figure 3 phase 2): after a BP step
  * every rank holds the selected branch id in `winner` (device int32, e.g. args->winner of

@@ -16,6 +16,14 @@
 struct lopa_bp {
   ncclComm_t comm;
   int32_t rank, world, device;
+  // peer-memory exchange (lopa_bp_step_p2p)
+  uint8_t* p2p_base = nullptr;      // local: [2 parities][world][rb] records, then [world] u32 flags
+  size_t p2p_rb = 0, p2p_bytes = 0;
+  int32_t p2p_b_loc = 0;
+  uint8_t* peer_base[32] = {};      // every rank's mapped base (own = p2p_base)
+  uint8_t** d_peer_base = nullptr;  // device copy of peer_base
+  bool p2p_open = false;
+  uint32_t epoch = 0;
 };
 
 extern "C" int lopa_bp_get_unique_id(void* unique_id_out) {
@@ -111,6 +119,111 @@ extern "C" int lopa_bp_check(lopa_bp_t* bp) {
 
 extern "C" void lopa_bp_destroy(lopa_bp_t* bp) {
   if (!bp) return;
+  if (bp->p2p_open)
+    for (int q = 0; q < bp->world; ++q)
+      if (q != bp->rank && bp->peer_base[q]) cudaIpcCloseMemHandle(bp->peer_base[q]);
+  if (bp->d_peer_base) cudaFree(bp->d_peer_base);
+  if (bp->p2p_base) cudaFree(bp->p2p_base);
   ncclCommDestroy(bp->comm);
   delete bp;
+}
+
+// ---- peer-memory exchange ---------------------------------------------------------------------
+static_assert(sizeof(cudaIpcMemHandle_t) == LOPA_BP_IPC_HANDLE_BYTES, "IPC handle size");
+
+namespace {
+// One CTA: copy this rank's record (rb bytes, 16-byte units) into slot `rank` of the current
+// parity of every peer, then, after a system-scope fence, raise this rank's flag to `epoch`
+// in every peer's flag array (release).
+__global__ void bp_publish_kernel(uint8_t* const* peer_base, int world, int rank, size_t rb,
+                                  size_t flags_off, int parity, uint32_t epoch) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // K2 has written this rank's record
+  asm volatile("griddepcontrol.launch_dependents;");
+  const size_t slot = ((size_t)parity * world + rank) * rb;
+  const uint4* src = reinterpret_cast<const uint4*>(peer_base[rank] + slot);
+  const size_t n16 = rb / 16;
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) continue;
+    uint4* dst = reinterpret_cast<uint4*>(peer_base[q] + slot);
+    for (size_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < world; ++q) {
+      uint32_t* f = reinterpret_cast<uint32_t*>(peer_base[q] + flags_off) + rank;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+    }
+  }
+}
+}  // namespace
+
+extern "C" int lopa_bp_p2p_alloc(lopa_bp_t* bp, int32_t window, int32_t b_loc, void* handle_out) {
+  if (!bp || !handle_out || b_loc < 1 || window < 1 || window > LOPA_MAX_WINDOW || bp->p2p_base)
+    return LOPA_ERR_INVALID_ARG;
+  if (cudaSetDevice(bp->device) != cudaSuccess) return LOPA_ERR_CUDA;
+  bp->p2p_rb = lopa_bp_record_bytes(window, b_loc);
+  bp->p2p_b_loc = b_loc;
+  const size_t flags_off = 2 * (size_t)bp->world * bp->p2p_rb;
+  bp->p2p_bytes = flags_off + 32 * sizeof(uint32_t);
+  if (cudaMalloc(&bp->p2p_base, bp->p2p_bytes) != cudaSuccess) return LOPA_ERR_CUDA;
+  if (cudaMemset(bp->p2p_base, 0, bp->p2p_bytes) != cudaSuccess) return LOPA_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, bp->p2p_base) != cudaSuccess) return LOPA_ERR_CUDA;
+  std::memcpy(handle_out, &h, sizeof(h));
+  return LOPA_OK;
+}
+
+extern "C" int lopa_bp_p2p_open(lopa_bp_t* bp, const void* all_handles) {
+  if (!bp || !all_handles || !bp->p2p_base || bp->p2p_open) return LOPA_ERR_INVALID_ARG;
+  if (cudaSetDevice(bp->device) != cudaSuccess) return LOPA_ERR_CUDA;
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(all_handles);
+  for (int q = 0; q < bp->world; ++q) {
+    if (q == bp->rank) {
+      bp->peer_base[q] = bp->p2p_base;
+      continue;
+    }
+    void* ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, hs[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+      return LOPA_ERR_CUDA;
+    bp->peer_base[q] = static_cast<uint8_t*>(ptr);
+  }
+  if (cudaMalloc(&bp->d_peer_base, 32 * sizeof(uint8_t*)) != cudaSuccess) return LOPA_ERR_CUDA;
+  if (cudaMemcpy(bp->d_peer_base, bp->peer_base, 32 * sizeof(uint8_t*), cudaMemcpyHostToDevice) !=
+      cudaSuccess)
+    return LOPA_ERR_CUDA;
+  bp->p2p_open = true;
+  return LOPA_OK;
+}
+
+extern "C" int lopa_bp_step_p2p(lopa_bp_t* bp, const lopa_step_args_t* args, int32_t b_loc,
+                                void* stream) {
+  if (!bp || !args || !bp->p2p_open || b_loc != bp->p2p_b_loc) return LOPA_ERR_INVALID_ARG;
+  if ((int64_t)b_loc * bp->world < args->max_branches) return LOPA_ERR_INVALID_ARG;
+  if (lopa_bp_record_bytes(args->window, b_loc) != bp->p2p_rb) return LOPA_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint32_t epoch = ++bp->epoch;
+  const int parity = (int)(epoch & 1u);
+  const size_t rb = bp->p2p_rb;
+  uint8_t* records = bp->p2p_base + (size_t)parity * bp->world * rb;
+  uint8_t* mine = records + rb * bp->rank;
+  int st = lopa::launch_bp_local(args, bp->rank * b_loc, b_loc, mine, s);
+  if (st != LOPA_OK) return st;
+  const size_t flags_off = 2 * (size_t)bp->world * rb;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, bp_publish_kernel, (uint8_t* const*)bp->d_peer_base, (int)bp->world,
+                           (int)bp->rank, rb, flags_off, parity, epoch) != cudaSuccess)
+      return LOPA_ERR_CUDA;
+  }
+  return lopa::launch_bp_finish(args, b_loc, bp->world, records, s,
+                                reinterpret_cast<const uint32_t*>(bp->p2p_base + flags_off), epoch);
 }

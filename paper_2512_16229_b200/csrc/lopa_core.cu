@@ -1141,9 +1141,25 @@ __global__ void verify_ex_kernel(const float* conf, const uint8_t* mask, const i
 // Global half of a BP step: one warp; lane r reads record r's header.
 template <int S>
 __global__ void bp_finish_kernel(const Params P, const uint8_t* records, int world, int b_loc,
-                                 int n_scores) {
+                                 int n_scores, const uint32_t* flags, uint32_t epoch) {
   __shared__ uint64_t keys[32 * S];
   const int lane = threadIdx.x;
+  grid_dep_wait();  // PDL (peer-memory path): the publisher before us has been issued
+  if (flags != nullptr) {
+    // peer-memory exchange (lopa_bp_step_p2p): wait until every rank's record of this epoch
+    // has landed (acquire at system scope pairs with the publisher's release); a rank that
+    // never arrives (bounded spin) is reported as LOPA_DEV_PEER_TIMEOUT instead of hanging
+    if (lane < world) {
+      uint32_t v = 0;
+      for (uint32_t spin = 0; spin < (1u << 26); ++spin) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + lane) : "memory");
+        if (v >= epoch) break;
+        __nanosleep(64);
+      }
+      if (v < epoch) atomicOr(P.dev_status, kDevPeerTimeout);
+    }
+    __syncwarp();
+  }
   const size_t rb = record_bytes(b_loc);
   float bs = -INFINITY;
   int bid = 0x7FFFFFFF;
@@ -1479,7 +1495,7 @@ int launch_step_decide(const lopa_step_args_t* a, cudaStream_t s) {
 }
 
 int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, const void* records,
-                     cudaStream_t s) {
+                     cudaStream_t s, const uint32_t* flags, uint32_t epoch) {
   if (!a || !records || b_loc < 1 || world < 1 || world > 32) return LOPA_ERR_INVALID_ARG;
   if (a->window < 1 || a->k < 0 || !(a->tau > 0.f && a->tau <= 1.f)) return LOPA_ERR_INVALID_ARG;
   if (!a->scores || !a->winner || !a->next_tokens || !a->next_mask || !a->n_branches_next ||
@@ -1491,13 +1507,24 @@ int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, co
   Workspace ws{};
   Params P = base_params(a, ws);
   const int n_scores = a->max_branches;
-  if (a->window > 64)
-    bp_finish_kernel<8><<<1, 32, 0, s>>>(P, static_cast<const uint8_t*>(records), world, b_loc,
-                                         n_scores);
-  else
-    bp_finish_kernel<2><<<1, 32, 0, s>>>(P, static_cast<const uint8_t*>(records), world, b_loc,
-                                         n_scores);
-  return cuda_status(cudaGetLastError());
+  auto kern = a->window > 64 ? bp_finish_kernel<8> : bp_finish_kernel<2>;
+  const uint8_t* rec = static_cast<const uint8_t*>(records);
+  if (flags == nullptr) {
+    kern<<<1, 32, 0, s>>>(P, rec, world, b_loc, n_scores, flags, epoch);
+    return cuda_status(cudaGetLastError());
+  }
+  // peer-memory path: launched programmatically dependent on the publisher (it waits for the
+  // flags anyway), so its launch overlaps the publish
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_status(cudaLaunchKernelEx(&cfg, kern, P, rec, world, b_loc, n_scores, flags, epoch));
 }
 
 }  // namespace lopa

@@ -15,6 +15,7 @@ namespace lopa {
 
 constexpr int kDevEmptyMask = 1;
 constexpr int kDevNonfinite = 2;
+constexpr int kDevPeerTimeout = 4;
 
 // Position state of one window held in registers.
 template <int S>

@@ -46,7 +46,7 @@ int num_sms(int device);
 inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? LOPA_OK : LOPA_ERR_CUDA; }
 
 int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, const void* records,
-                     cudaStream_t s);
+                     cudaStream_t s, const uint32_t* flags = nullptr, uint32_t epoch = 0);
 int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_loc, void* record,
                     cudaStream_t s);
 int validate_step_args(const lopa_step_args_t* a, bool need_next, bool need_logits = true);

@@ -26,6 +26,8 @@ METRIC_SLIDING_MIN = 1     # P:204 sliding window
 METRIC_BOTTOM_FRACTION = 2 # P:204 least-confident segment
 DEV_EMPTY_MASK = 1
 DEV_NONFINITE = 2
+DEV_PEER_TIMEOUT = 4
+IPC_HANDLE_BYTES = 64
 MAX_WINDOW = 256
 MAX_BRANCHES = 32
 MAX_ROWS = 4096
@@ -82,6 +84,9 @@ _SIGS = {
     "lopa_bp_create": (_i32, [_c_void_p, _i32, _i32, _i32, ctypes.POINTER(_c_void_p)]),
     "lopa_bp_step": (_i32, [_c_void_p, ctypes.POINTER(StepArgs), _i32, _c_void_p, _c_void_p]),
     "lopa_bp_check": (_i32, [_c_void_p]),
+    "lopa_bp_p2p_alloc": (_i32, [_c_void_p, _i32, _i32, _c_void_p]),
+    "lopa_bp_p2p_open": (_i32, [_c_void_p, _c_void_p]),
+    "lopa_bp_step_p2p": (_i32, [_c_void_p, ctypes.POINTER(StepArgs), _i32, _c_void_p]),
     "lopa_bp_commit_winner": (_i32, [_c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p, _c_void_p]),
     "lopa_bp_destroy": (None, [_c_void_p]),
     "lopa_debug_timeline": (_i32, [_c_void_p, _i32]),
@@ -458,7 +463,9 @@ class BranchParallel:
 
     The NCCL unique id is created by rank 0 and shipped over the given torch process group."""
 
-    def __init__(self, stepper: Stepper, rank: int, world: int, group=None):
+    def __init__(self, stepper: Stepper, rank: int, world: int, group=None, p2p: bool = False):
+        """p2p=True: exchange the records over peer memory (lopa_bp_step_p2p: CUDA IPC mappings
+        of every rank's record buffer, NVLink stores + epoch flags) instead of ncclAllGather."""
         import torch.distributed as dist
         self.s, self.rank, self.world = stepper, rank, world
         self.b_loc, self.lo, self.hi = bp_shard(stepper.max_branches, world, rank)
@@ -484,6 +491,18 @@ class BranchParallel:
         self.conf = torch.full((self.b_loc, W), float("nan"), dtype=torch.float32, device=d)
         self.argmax = torch.full((self.b_loc, W), -1, dtype=torch.int32, device=d)
         self.scores = torch.empty(world * self.b_loc, dtype=torch.float32, device=d)
+        self.p2p = p2p
+        if p2p:
+            hbuf = (ctypes.c_uint8 * IPC_HANDLE_BYTES)()
+            _check(lib().lopa_bp_p2p_alloc(self.h, W, self.b_loc, hbuf), "lopa_bp_p2p_alloc")
+            mine = bytes(hbuf)
+            if world > 1:
+                allh = [None] * world
+                dist.all_gather_object(allh, mine, group=group)
+            else:
+                allh = [mine]
+            raw_all = (ctypes.c_uint8 * (IPC_HANDLE_BYTES * world))(*b"".join(allh))
+            _check(lib().lopa_bp_p2p_open(self.h, raw_all), "lopa_bp_p2p_open")
 
     def step(self, local_logits, n_branches, branch_tokens, branch_mask) -> StepOutputs:
         """local_logits: this rank's bf16 [b_loc][W][ld]; tables are the full replicated ones."""
@@ -492,8 +511,12 @@ class BranchParallel:
         a.conf, a.argmax = self.conf.data_ptr(), self.argmax.data_ptr()
         a.workspace, a.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
         a.scores = self.scores.data_ptr()
-        _check(lib().lopa_bp_step(self.h, ctypes.byref(a), self.b_loc, _p(self.records),
-                                  _stream(s.device)), "lopa_bp_step")
+        if self.p2p:
+            _check(lib().lopa_bp_step_p2p(self.h, ctypes.byref(a), self.b_loc, _stream(s.device)),
+                   "lopa_bp_step_p2p")
+        else:
+            _check(lib().lopa_bp_step(self.h, ctypes.byref(a), self.b_loc, _p(self.records),
+                                      _stream(s.device)), "lopa_bp_step")
         return s.out
 
     def commit_winner(self, local_payloads: torch.Tensor, out: torch.Tensor | None = None,

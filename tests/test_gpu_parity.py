@@ -391,6 +391,36 @@ def test_bp_nccl_single_rank(L):
         bp.close()
 
 
+def test_bp_p2p_single_rank(L):
+    """The peer-memory exchange (lopa_bp_step_p2p: records written into every rank's mapped
+    buffer, epoch flags released at system scope, double-buffered by parity) with one rank:
+    five consecutive steps identical to lopa_step, no peer timeout."""
+    V, W, k, tau = 151936, 32, 7, 0.9
+    st = L.Stepper(V, W, k + 1, k, tau, DEV)
+    st2 = L.Stepper(V, W, k + 1, k, tau, DEV)
+    bp = L.BranchParallel(st2, 0, 1, p2p=True)
+    try:
+        tok, msk, nb = G.fresh_tables(k, W, DEV)
+        logits = torch.zeros((k + 1, W, st.ld), dtype=torch.bfloat16, device=DEV)
+        for it in range(5):
+            n = int(nb.item())
+            L.syn_generate(9, 0, V, tok, msk, n_branches=n, out=logits[:n])
+            ref = st.step(logits, nb, tok, msk)
+            o2 = bp.step(logits, nb, tok, msk)
+            torch.cuda.synchronize()
+            assert int(o2.status.item()) == 0
+            assert (o2.winner.item(), o2.n_next.item()) == (ref.winner.item(), ref.n_next.item())
+            m = int(ref.n_next.item())
+            assert torch.equal(o2.next_tokens[:m], ref.next_tokens[:m])
+            assert torch.equal(o2.next_mask[:m], ref.next_mask[:m])
+            if m == 0:
+                break
+            tok, msk, nb = ref.next_tokens.clone(), ref.next_mask.clone(), ref.n_next.clone()
+        bp.check()
+    finally:
+        bp.close()
+
+
 @pytest.mark.parametrize("nbytes", [16, 4096, 1835008])
 def test_bp_commit_winner_single_rank(L, nbytes):
     """NEXT-3 Commit-Winner-Cache over the real NCCL path (one rank): the winner's payload
