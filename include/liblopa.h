@@ -298,7 +298,9 @@ int lopa_bp_commit_winner(lopa_bp_t* bp, const int32_t* winner, int32_t b_loc,
  * tolerance against the exact (fp64) definition.
  *   hidden   device bf16 [rows][ld_hidden], 16-byte aligned, ld_hidden % 8 == 0
  *   weight   device bf16 [vocab][ld_weight] (nn.Linear layout: one row per token), same rules
- *   rows in [1, 256]; hidden_dim a positive multiple of 64; vocab in [1, LOPA_MAX_VOCAB]
+ *   rows in [1, LOPA_MAX_ROWS]; hidden_dim a positive multiple of 64; vocab in
+ *     [1, LOPA_MAX_VOCAB].  Up to 256 rows share one pass over the weights; more rows run in
+ *     chunks of 256, one pass each.
  *   row_mask device uint8 [rows] or NULL: rows with row_mask[r] == 0 get conf NaN, argmax -1
  *   conf, argmax  device [rows]; a selected row whose logits contain NaN or +inf, or are all
  *            -inf, sets LOPA_DEV_NONFINITE (conf NaN, argmax -1); -inf logits are tokens of
@@ -314,7 +316,7 @@ int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, const void* we
 
 /* The verify step of lopa_step (a1 -> a2 -> a3 -> a4) from the verify forward's HIDDEN STATES
  * instead of its logits: a1 is the fused LM-head + Conf above over the max_branches * window
- * rows (<= 256) of `hidden` (bf16 [max_branches][window][ld_hidden], row b * window + i =
+ * rows (<= LOPA_MAX_ROWS) of `hidden` (bf16 [max_branches][window][ld_hidden], row b * window + i =
  * branch b, position i), restricted to the masked rows of present branches; then the same
  * decision kernel as lopa_step.  args->logits and args->ld are ignored; every other field of
  * `args` keeps its lopa_step meaning (conf / argmax receive the fused a1 results).

@@ -140,6 +140,7 @@ struct Args {
   const uint8_t* row_mask;     // nullable: rows with row_mask[r] == 0 are not reported
   const int32_t* n_branches;   // nullable: rows r with r / window >= *n_branches are not reported
   int32_t window;
+  int32_t row_base;            // global index of this launch's row 0 (rows > 256 run in chunks)
 };
 
 // The vocabulary units of CTA b: [u0, u1) with u = floor(b * n_units / G).
@@ -371,7 +372,8 @@ __global__ void __launch_bounds__(256) lopa_lmhead_fold_kernel(const Args A, int
   const int row = (int)(blockIdx.x * 8 + (threadIdx.x >> 5));
   const int lane = threadIdx.x & 31;
   if (row >= A.M) return;
-  const bool valid = (!A.row_mask || A.row_mask[row] != 0) && (!A.n_branches || row / A.window < *A.n_branches);
+  const bool valid = (!A.row_mask || A.row_mask[row] != 0) &&
+                     (!A.n_branches || (A.row_base + row) / A.window < *A.n_branches);
   if (!valid) {  // not a row of the step: untouched semantics of a1 (conf NaN, argmax -1)
     if (lane == 0) {
       A.conf[row] = NAN;
@@ -462,10 +464,11 @@ extern "C" size_t lopa_lmhead_workspace_bytes(int32_t rows) {
   return (size_t)lmh::kMaxGrid * lmh::kMaxRows * sizeof(float4);
 }
 
-static int launch_lmhead(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
-                         int32_t rows, int32_t hidden_dim, int32_t vocab, const uint8_t* row_mask,
-                         const int32_t* n_branches, int32_t window, float* conf, int32_t* argmax,
-                         int32_t* dev_status, void* workspace, size_t workspace_bytes, void* stream) {
+static int launch_lmhead_chunk(const void* hidden, int64_t ld_hidden, const void* weight,
+                               int64_t ld_weight, int32_t rows, int32_t hidden_dim, int32_t vocab,
+                               const uint8_t* row_mask, const int32_t* n_branches, int32_t window,
+                               int32_t row_base, float* conf, int32_t* argmax, int32_t* dev_status,
+                               void* workspace, size_t workspace_bytes, void* stream) {
   if (!hidden || !weight || !conf || !argmax || !dev_status || !workspace) return LOPA_ERR_INVALID_ARG;
   if (rows < 1 || rows > lmh::kMaxRows || vocab < 1 || vocab > LOPA_MAX_VOCAB || hidden_dim < lmh::kBK ||
       hidden_dim % lmh::kBK != 0)
@@ -506,6 +509,7 @@ static int launch_lmhead(const void* hidden, int64_t ld_hidden, const void* weig
   a.row_mask = row_mask;
   a.n_branches = n_branches;
   a.window = window < 1 ? 1 : window;
+  a.row_base = row_base;
   const int G = lmh::grid_for(device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   lmh::lopa_lmhead_kernel<<<G, lmh::kThreads, lmh::kSmemBytes, s>>>(ma, mb256, mb16, a);
@@ -525,6 +529,25 @@ static int launch_lmhead(const void* hidden, int64_t ld_hidden, const void* weig
   return e == cudaSuccess ? LOPA_OK : LOPA_ERR_CUDA;
 }
 
+// Rows beyond 256 (e.g. k = 14: 15 branches x 32 positions) run in chunks of 256 rows, each a
+// full pass over the weights (stream-ordered; the workspace is reused).
+static int launch_lmhead(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                         int32_t rows, int32_t hidden_dim, int32_t vocab, const uint8_t* row_mask,
+                         const int32_t* n_branches, int32_t window, float* conf, int32_t* argmax,
+                         int32_t* dev_status, void* workspace, size_t workspace_bytes, void* stream) {
+  if (rows < 1 || rows > LOPA_MAX_ROWS || !hidden) return LOPA_ERR_INVALID_ARG;
+  for (int32_t r0 = 0; r0 < rows; r0 += lmh::kMaxRows) {
+    const int32_t rc = rows - r0 < lmh::kMaxRows ? rows - r0 : lmh::kMaxRows;
+    const int st = launch_lmhead_chunk(
+        static_cast<const uint16_t*>(hidden) + (size_t)r0 * ld_hidden, ld_hidden, weight, ld_weight,
+        rc, hidden_dim, vocab, row_mask ? row_mask + r0 : nullptr, n_branches, window, r0,
+        conf ? conf + r0 : nullptr, argmax ? argmax + r0 : nullptr, dev_status, workspace,
+        workspace_bytes, stream);
+    if (st != LOPA_OK) return st;
+  }
+  return LOPA_OK;
+}
+
 extern "C" int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, const void* weight,
                                       int64_t ld_weight, int32_t rows, int32_t hidden_dim,
                                       int32_t vocab, const uint8_t* row_mask, float* conf,
@@ -541,7 +564,7 @@ extern "C" int lopa_step_lmhead(const lopa_step_args_t* a, const void* hidden, i
   int st = validate_step_args(a, true, false);
   if (st != LOPA_OK) return st;
   const int64_t rows = (int64_t)a->max_branches * a->window;
-  if (rows > lmh::kMaxRows) return LOPA_ERR_UNSUPPORTED;
+  if (rows > LOPA_MAX_ROWS) return LOPA_ERR_UNSUPPORTED;
   st = launch_lmhead(hidden, ld_hidden, weight, ld_weight, (int32_t)rows, hidden_dim, a->vocab,
                      a->branch_mask, a->n_branches, a->window, a->conf, a->argmax, a->dev_status,
                      lmh_workspace, lmh_workspace_bytes, stream);

@@ -191,7 +191,8 @@ def confidence(logits: torch.Tensor, vocab: int | None = None, row_mask: torch.T
 class LMHead:
     """LM-head projection with Conf fused into the GEMM epilogue (tcgen05): conf / argmax of
     each row of ``hidden`` (bf16 [rows][K]) against ``weight`` (bf16 [V][K]) without
-    materialising the logits.  Owns its workspace; rows <= 256, K % 64 == 0."""
+    materialising the logits.  Owns its workspace; rows <= max_rows <= 4096 (256 rows per pass
+    over the weights), K % 64 == 0."""
 
     def __init__(self, weight: torch.Tensor, max_rows: int = 256):
         _need_cuda(weight)

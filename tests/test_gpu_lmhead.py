@@ -27,7 +27,7 @@ def _dev(u16):
 
 
 def _check(L, h, W, rows=None, stats=None):
-    head = L.LMHead(_dev(W))
+    head = L.LMHead(_dev(W), max_rows=max(256, h.shape[0]))
     c, a, st = head(_dev(h))
     torch.cuda.synchronize()
     assert int(st.item()) == 0
@@ -52,8 +52,10 @@ def _check(L, h, W, rows=None, stats=None):
 
 @pytest.mark.parametrize("M,K,V", [(1, 64, 16), (7, 64, 100), (33, 128, 1000), (128, 256, 4096),
                                    (129, 64, 8200), (200, 192, 4111), (256, 128, 16),
-                                   (256, 320, 5000), (64, 3584, 2048)])
+                                   (256, 320, 5000), (64, 3584, 2048), (300, 128, 3000),
+                                   (600, 64, 1000)])
 def test_lmhead_shapes(L, M, K, V):
+    """Rows > 256 run in chunks of 256 rows (one pass over the weights each)."""
     h, W, _ = syngen.lmhead_inputs(M * 7 + V, M, K, V)
     st = []
     _check(L, h, W, stats=st)
@@ -108,7 +110,8 @@ def _oracle_decisions(conf, amax, tok, msk, n, k, tau):
 
 
 @pytest.mark.parametrize("seed,V,K,W,k", [(0, 5000, 128, 32, 7), (1, 20000, 256, 16, 3),
-                                          (2, 3000, 64, 64, 3), (3, 151936, 3584, 32, 7)])
+                                          (2, 3000, 64, 64, 3), (3, 151936, 3584, 32, 7),
+                                          (4, 8000, 128, 32, 14)])
 def test_step_lmhead(L, seed, V, K, W, k):
     """lopa_step_lmhead (fused LM-head a1 + the step's a2-a4) against the oracle: conf within
     R27, and every decision exactly the oracle's decision on the GPU's own conf (and on the
