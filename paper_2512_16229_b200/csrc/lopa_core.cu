@@ -1,26 +1,32 @@
-// liblopa core: the fused vocabulary reduction (a1) with its last-CTA decision tail (a2-a4), the
-// standalone decision kernels and the C-ABI entry points.
+// liblopa core: the vocabulary reduction K1 (a1), the fold + decision kernel K2 (a1 fold,
+// a2-a4), the standalone decision kernels and the C-ABI entry points.  DESIGN.md §5.
 //
-// Fused kernel design:
-//   * Persistent grid, one CTA per SM.  The masked (branch, position) rows are compacted
-//     in-kernel from the masks (no host sync).  A row of V logits is cut into canonical
-//     segments (<= 8192 elements, 16 KB) and segments into canonical groups of kSegPerItem.
-//   * Work items are (row, group) pairs, handed out dynamically: CTA b starts with item b, then
-//     takes the next item from a global counter (prefetched one item ahead), so faster SMs
-//     take more work and all CTAs finish within about one item.
-//   * Warp 0 lane 0 is the TMA producer: one cp.async.bulk per segment into a kStages-deep ring
-//     of 16 KB shared-memory stages, mbarrier transaction-byte completion, L2 evict-first (each
-//     logit is read exactly once).  The stage's (row, segment) tag travels in shared memory.
-//   * kConsumerWGs consumer warpgroups take stages round-robin; the 4 warps of a group each
-//     reduce a fixed interleaved quarter of the segment with 128-bit shared loads: exact max
-//     (max.bf16x2), sum of exp2((x - m) log2 e) with x - m formed exactly by fma.f32.bf16 and
-//     packed f32x2 multiplies/adds in a fixed order, exact first argmax.
-//   * The warp that completes an item folds its 4 x kSegPerItem warp partials (fixed order) into
-//     one group partial in the workspace.  No global atomics per row or per segment.
-//   * The last CTA to finish (one counter) folds every row's group partials in fixed order
-//     (conf bits depend only on the row's bytes), then runs the tail with all its threads:
-//     Eq. 2 scores + select, Eq. 1 anchor, top-k spawn (MODE_STEP) or the local branch-parallel
-//     record (MODE_BP_LOCAL).
+// K1 lopa_reduce_kernel (persistent, one CTA per SM but one left to K2):
+//   * A row of V logits is cut into canonical segments (<= 8192 elements, 16 KB) and segments
+//     into groups of kSegPerItem = 2; a work item is one (group, row) = ONE cp.async.bulk of
+//     <= 32 KB into a kStages-deep ring, mbarrier transaction bytes, L2 evict-first.  Items are
+//     numbered group-major so the short last group of every row streams at the very end.
+//   * CTA b takes items b and G + b (the first one issued before the row masks arrive), then
+//     claims items from a global counter, two claims in flight; unmasked rows are skipped.
+//   * kConsumerWGs consumer warpgroups share the stages (warpgroup w: segment w % 2 of the
+//     stages of phase w / 2); each warp reduces an interleaved quarter of its segment with
+//     128-bit shared loads: exact max (max.NaN.bf16x2), sum of exp2((x - m) log2 e) with x - m
+//     formed exactly by fma.f32.bf16 and packed f32x2 multiplies/adds in a fixed order, exact
+//     first argmax; the stage is released once the registers hold it.
+//   * The warp completing an item folds its warp partials (fixed order) into one group partial
+//     in the workspace ([n_grp][n_cand], group-major).  No atomics per row or segment.
+// K2 lopa_tail_kernel<MODE, S> (one CTA, programmatic dependent launch on K1's free SM): stages
+//   the tables and builds the masked-row list while K1 streams; after griddepcontrol.wait it
+//   bulk-copies the group partials into shared memory, folds each row in a fixed 16-slot tree
+//   (conf bits depend only on the row's bytes), then Eq. 2 + select, Eq. 1 anchor and the
+//   top-k spawn (MODE_STEP / MODE_DECIDE) or the branch-parallel record (MODE_BP_LOCAL).
+//
+// Compile-time knobs (A/B builds via build.py --variant; defaults are the measured best):
+//   LOPA_STAGES, LOPA_WGS, LOPA_CTAS_PER_SM, LOPA_CLAIM_AHEAD, LOPA_SEG_ELEMS,
+//   LOPA_SEG_PER_ITEM, LOPA_MBAR_SUSPEND_NS, LOPA_TAIL_THREADS, LOPA_POLY_WORDS (exp2 on the FMA
+//   pipe), LOPA_LATE_ARGMAX; experiments only: LOPA_NOCOMPUTE (streaming without arithmetic),
+//   LOPA_EXP_NOARGMAX, LOPA_NO_PDL, LOPA_NO_TLB_WARM; LOPA_TIMELINE (per-CTA %globaltimer
+//   stamps read by scripts/timeline.py).
 #include <algorithm>
 #include <cstdio>
 #include <cstring>

@@ -161,3 +161,20 @@ def test_step_lmhead(L, seed, V, K, W, k):
     srt = sorted(r_scores, reverse=True)
     if len(srt) < 2 or srt[0] - srt[1] > 2 * tol.max():
         assert int(out.winner.item()) == r_w
+
+
+def test_lmhead_row_mask(L):
+    """Rows with row_mask = 0 are not reported (conf NaN, argmax -1) and never flag the status;
+    the selected rows equal the unmasked call's."""
+    h, W, _ = syngen.lmhead_inputs(12, 50, 128, 900)
+    head = L.LMHead(_dev(W))
+    hd = _dev(h)
+    c0, a0, _ = head(hd)
+    c0, a0 = c0.clone(), a0.clone()
+    rm = torch.from_numpy((np.arange(50) % 3 != 0).astype(np.uint8)).to(DEV)
+    c1, a1, st = head(hd, row_mask=rm)
+    torch.cuda.synchronize()
+    sel = rm.bool()
+    assert int(st.item()) == 0
+    assert torch.equal(c1[sel], c0[sel]) and torch.equal(a1[sel], a0[sel])
+    assert torch.isnan(c1[~sel]).all() and (a1[~sel] == -1).all()
