@@ -16,7 +16,12 @@
  *   a4  Alg. 1 step 2: top-k of M_{B0} by (conf desc, position asc) (R6),
  *       n_br = min(k, |M_{B0}|) + 1 (R7); B_j = B0 with p_j filled by its greedy token.
  *   a5  Branch parallelism: branches sharded over ranks, one NCCL all-gather of
- *       each rank's local best (score, id, row) per step.
+ *       each rank's local best (score, id, row) per step (or, opt-in, the same exchange over
+ *       CUDA-IPC peer memory: lopa_bp_step_p2p).
+ * Beyond the step: windows of up to 256 positions with per-position Eq. 1
+ * thresholds (the D2F multi-block window, NEXT-1), Eq. 2 variants (NEXT-2), the winner's
+ * payload exchange (Commit-Winner-Cache, NEXT-3) and the LM-head projection on tcgen05 with
+ * Conf fused into its epilogue (NEXT-4).
  *
  * Conventions (all calls):
  *   - Pointers named *_dev / documented "device" are device pointers into caller-owned
