@@ -17,6 +17,10 @@ relative error ~K·2^-53), then conf = 1 / sum_v exp(l_v - max l), argmax = lowe
 |l~_rv - l_rv| <= K·2^-23·sum_k |h_rk W_vk| (the classical bound for a K-term fp32 sum of
 exact products, any order); a conf computed from logits that are each within E of the
 exact ones lies within conf·(exp(2E) - 1) of the exact conf.
+
+Parity pins: tests/test_oracle_lmhead.py — one-hot hidden rows reduce to the pinned row Conf,
+exact rational logits with 50-digit exp sums, ties, non-finite rows, the error bound checked
+against real fp32 evaluations, the conf perturbation bound.  No function is "parity unpinned".
 """
 from __future__ import annotations
 
