@@ -29,6 +29,11 @@ tau_act, tau_conf; Appendix table).  The block semantics are SPEC's st
   committed columns are dropped (identical in every branch, since every branch extends
   B* there), newly activated columns are appended fully masked.  If the step completed the
   window (R21) the next forward is the new window's initial predict (a0, R17).
+
+Parity pins: tests/test_oracle_d2f.py — SPEC's block examples, the single-block
+reduction to the pinned Alg. 1 loop (block_size >= L_gen), the tau_add = 1
+reduction to the sequential per-block loop, the one-hot two-block trace
+and the pipeline invariants.  No function here is "parity unpinned".
 """
 from __future__ import annotations
 
