@@ -44,6 +44,8 @@ CONFIGS = {
 # output projection K = 3584 (Qwen2.5-7B hidden size; outside the paper), one GPU
 CONFIGS["lmhead-dream"] = dict(V=151936, W=32, k=7, tau=0.9, K=3584,
                                name="D2F-Dream verify step from hidden states: fused LM head K=3584 V=151936 W=32 k=7 tau=0.9")
+CONFIGS["lmhead-gsm8k"] = dict(V=151936, W=32, k=14, tau=0.9, K=3584,
+                               name="D2F-Dream GSM8K (k=14, PAPER.md:528) verify step from hidden states: fused LM head, 480 rows in two 256-row passes")
 # NEXT-1: D2F multi-block windows (2, 4 and 8 active blocks of 32)
 for _k, _w in ((7, 64), (7, 128), (3, 256), (7, 256)):
     CONFIGS[f"d2f-k{_k}-w{_w}"] = dict(V=151936, W=_w, k=_k, tau=0.9,
