@@ -91,7 +91,7 @@ namespace lopa {
 #ifndef LOPA_CTAS_PER_SM
 #define LOPA_CTAS_PER_SM 1
 #endif
-constexpr int kStages = LOPA_STAGES;      // TMA ring depth (16 KB stages)
+constexpr int kStages = LOPA_STAGES;      // TMA ring depth (one <= 32 KB work item per stage)
 constexpr int kConsumerWGs = LOPA_WGS;    // consumer warpgroups per CTA
 constexpr int kThreads = 32 + 128 * kConsumerWGs;
 constexpr int kWarps = kThreads / 32;
@@ -450,8 +450,8 @@ __device__ __forceinline__ FoldAcc fold_tree16(int n, const float4 (&q)[16]) {
   return FoldAcc{M, t[0], a};
 }
 
-// ------------------------------------------------------------------ last-CTA tail
-// Everything the decision tail needs, staged in the (idle) TMA ring of the last CTA.
+// ------------------------------------------------------------------ K2's decision tail
+// Everything the decision tail needs, staged in K2's shared memory.
 constexpr int kScoreWarps = 8;  // warps scoring branches in the tail
 struct TailSmem {
   float conf[LOPA_MAX_ROWS];
@@ -597,7 +597,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
   TL(13);
 }
 
-// Local half of a BP step with all threads of the last CTA: local Eq. 2 scores, local best
+// Local half of a BP step with all threads of K2: local Eq. 2 scores, local best
 // (smallest local j with the largest score), and the exchange record.
 template <int NT, int S>
 __device__ void cta_tail_bp_local(const Params& P, TailSmem& T, int tid, int nb) {
