@@ -69,6 +69,26 @@ def test_confidence_rows(L, V):
     assert np.array_equal(amax.cpu().numpy(), ra)
 
 
+@pytest.mark.parametrize("V", [(1 << 20) + 3, 1 << 23])
+def test_confidence_huge_vocab(L, V):
+    """Up to LOPA_MAX_VOCAB = 2^23: 512 groups per row, so the fold takes its sequential
+    (> 16 groups) path; ragged tail at 2^20 + 3."""
+    rng = np.random.default_rng(V)
+    ld = ((V + 7) // 8) * 8
+    rnd = _bits(rng.standard_normal((3, V), dtype=np.float32) * np.float32(2))
+    rows = np.concatenate([special_rows(V), rnd])
+    buf = np.zeros((rows.shape[0], ld), np.uint16)
+    buf[:, :V] = rows
+    buf[:, V:] = 0x7FC0
+    t = torch.from_numpy(buf.view(np.int16)).to(DEV).view(torch.bfloat16)
+    conf, amax, st = L.confidence(t, vocab=V)
+    rc, ra, rst = O.confidence(rows)
+    assert int(st.item()) == rst == 0
+    c = conf.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(c - rc)) <= G.CONF_TOL
+    assert np.array_equal(amax.cpu().numpy(), ra)
+
+
 def test_confidence_row_mask_and_nonfinite(L):
     V = 3000
     rows = np.zeros((6, V), np.float32)
