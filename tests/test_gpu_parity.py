@@ -273,6 +273,13 @@ def _run_steps(L, seed, V, W, k, tau, iters, extras, blk=0, counter=None, metric
     return iters
 
 
+@pytest.mark.parametrize("V,W,k", [(300000, 8, 2), (1 << 21, 4, 1)])
+def test_step_many_groups(L, V, W, k):
+    """Vocabularies with more than 16 groups per row (19 and 128 groups): the decision kernel
+    folds them without staging, through the sequential fold."""
+    _run_steps(L, 5, V, W, k, 0.9, 3, extras=0)
+
+
 @pytest.mark.parametrize("seed", range(0, 120))
 def test_step_toy(L, seed):
     """Toy config (BASELINE configs[0]): V=64, W=8, k=2, tau=0.9, with tie / flat rows, iterated
