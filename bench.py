@@ -157,16 +157,18 @@ def cpu_baseline_oracle(full, tok, msk, nb, k, tau, budget_s=12.0):
     """The oracle as it stands (NumPy fp64, single thread) on whole verify steps of the same
     workload, repeated until ~budget_s of CPU time."""
     from oracle import lopa_oracle as O
+    from threadpoolctl import threadpool_limits
     n = int(nb.item())
     L16 = full.view(torch.int16).cpu().numpy().view(np.uint16)[:n]
     t_np, m_np = tok.cpu().numpy()[:n], msk.cpu().numpy()[:n]
     reps, t0 = 0, time.perf_counter()
-    while True:
-        O.step(L16, t_np, m_np, k, tau)
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s:
-            break
+    with threadpool_limits(limits=1):  # the stated core count: one thread
+        while True:
+            O.step(L16, t_np, m_np, k, tau)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s:
+                break
     return {"value": reps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{reps} full verify steps (n_br={n}, {int(m_np.sum())} masked rows x V=151936) "
                       f"in {el:.1f} s, NumPy fp64 single thread"}
@@ -207,12 +209,14 @@ def run_reference(args):
         a = O.anchor_fill(c[w], np.zeros(W, np.int64), tok[w], msk[w], tau)
         O.spawn_branches(c[w], np.zeros(W, np.int64), a.tokens, a.mask, k)
 
-    for _ in range(args.warmup):
-        one()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        one()
-    el = time.perf_counter() - t0
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):  # the stated core count: one thread
+        for _ in range(args.warmup):
+            one()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            one()
+        el = time.perf_counter() - t0
     f = n_s / len(rows)
     value = args.steps * f / el                     # full verify steps per second
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
