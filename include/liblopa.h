@@ -268,16 +268,30 @@ int lopa_syn_generate(uint64_t seed, int32_t block, int32_t vocab, int64_t ld, i
  * waits for every rank's flag of this step (acquire) and runs the same deterministic select /
  * anchor / spawn.  Records are double-buffered by epoch parity, so a rank may run one step
  * ahead of a slow reader.  Same results as lopa_bp_step.
- *   lopa_bp_p2p_alloc: allocates this rank's buffers for (window <= 256, b_loc) and writes
- *     its IPC handle (LOPA_BP_IPC_HANDLE_BYTES) to handle_out; call once per communicator.
+ *   lopa_bp_p2p_alloc: allocates this rank's buffers for (window <= 256, b_loc) and, if
+ *     payload_bytes > 0 (a multiple of 16), two parities of [b_loc][payload_bytes] payload
+ *     slots; writes its IPC handle (LOPA_BP_IPC_HANDLE_BYTES) to handle_out; once per
+ *     communicator.
  *   lopa_bp_p2p_open: all_handles = the world handles in rank order (gathered by the caller);
  *     maps every peer's buffers.
  *   lopa_bp_step_p2p: as lopa_bp_step (args, b_loc), on the P2P buffers.
  * Errors: LOPA_ERR_INVALID_ARG (order of calls, sizes), LOPA_ERR_CUDA (allocation, IPC). */
 #define LOPA_BP_IPC_HANDLE_BYTES 64
-int lopa_bp_p2p_alloc(lopa_bp_t* bp, int32_t window, int32_t b_loc, void* handle_out);
+int lopa_bp_p2p_alloc(lopa_bp_t* bp, int32_t window, int32_t b_loc, size_t payload_bytes,
+                      void* handle_out);
 int lopa_bp_p2p_open(lopa_bp_t* bp, const void* all_handles);
 int lopa_bp_step_p2p(lopa_bp_t* bp, const lopa_step_args_t* args, int32_t b_loc, void* stream);
+
+/* NEXT-3 over peer memory (Commit-Winner-Cache, without a collective): step e's
+ * payloads (e.g. each local branch's KV features) are written by their owner into its payload
+ * slots of parity e & 1 (lopa_bp_payload_slots: device pointer [b_loc][payload_bytes], NULL if
+ * none) before that rank's lopa_bp_step_p2p(e); after it, lopa_bp_commit_winner_p2p copies the
+ * winner's payload straight from its owner's slots into `out` (device, payload_bytes, 16-byte
+ * aligned): one pass over NVLink, ordered by the step's acquire of the owner's flag.  The
+ * parity double-buffering makes it safe for an owner to write step e + 1's payloads while
+ * peers still pull step e's. */
+void* lopa_bp_payload_slots(lopa_bp_t* bp, int32_t parity);
+int lopa_bp_commit_winner_p2p(lopa_bp_t* bp, const int32_t* winner, void* out, void* stream);
 
 /* NEXT-3 — Commit-Winner-Cache (Figure 3 phase 2): after a BP step
  * every rank holds the selected branch id in `winner` (device int32, e.g. args->winner of

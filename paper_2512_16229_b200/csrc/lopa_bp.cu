@@ -20,6 +20,8 @@ struct lopa_bp {
   uint8_t* p2p_base = nullptr;      // local: [2 parities][world][rb] records, then [world] u32 flags
   size_t p2p_rb = 0, p2p_bytes = 0;
   int32_t p2p_b_loc = 0;
+  size_t p2p_payload = 0;           // payload bytes per branch (0: none)
+  size_t p2p_payload_off = 0;       // [2 parities][b_loc][payload] after the flags
   uint8_t* peer_base[32] = {};      // every rank's mapped base (own = p2p_base)
   uint8_t** d_peer_base = nullptr;  // device copy of peer_base
   bool p2p_open = false;
@@ -158,14 +160,18 @@ __global__ void bp_publish_kernel(uint8_t* const* peer_base, int world, int rank
 }
 }  // namespace
 
-extern "C" int lopa_bp_p2p_alloc(lopa_bp_t* bp, int32_t window, int32_t b_loc, void* handle_out) {
-  if (!bp || !handle_out || b_loc < 1 || window < 1 || window > LOPA_MAX_WINDOW || bp->p2p_base)
+extern "C" int lopa_bp_p2p_alloc(lopa_bp_t* bp, int32_t window, int32_t b_loc, size_t payload_bytes,
+                                 void* handle_out) {
+  if (!bp || !handle_out || b_loc < 1 || window < 1 || window > LOPA_MAX_WINDOW || bp->p2p_base ||
+      payload_bytes % 16 != 0)
     return LOPA_ERR_INVALID_ARG;
   if (cudaSetDevice(bp->device) != cudaSuccess) return LOPA_ERR_CUDA;
   bp->p2p_rb = lopa_bp_record_bytes(window, b_loc);
   bp->p2p_b_loc = b_loc;
   const size_t flags_off = 2 * (size_t)bp->world * bp->p2p_rb;
-  bp->p2p_bytes = flags_off + 32 * sizeof(uint32_t);
+  bp->p2p_payload = payload_bytes;
+  bp->p2p_payload_off = flags_off + 256;
+  bp->p2p_bytes = bp->p2p_payload_off + 2 * (size_t)b_loc * payload_bytes;
   if (cudaMalloc(&bp->p2p_base, bp->p2p_bytes) != cudaSuccess) return LOPA_ERR_CUDA;
   if (cudaMemset(bp->p2p_base, 0, bp->p2p_bytes) != cudaSuccess) return LOPA_ERR_CUDA;
   cudaIpcMemHandle_t h;
@@ -226,4 +232,51 @@ extern "C" int lopa_bp_step_p2p(lopa_bp_t* bp, const lopa_step_args_t* args, int
   }
   return lopa::launch_bp_finish(args, b_loc, bp->world, records, s,
                                 reinterpret_cast<const uint32_t*>(bp->p2p_base + flags_off), epoch);
+}
+
+// ---- Commit-Winner-Cache over peer memory ---------------------------------------------------------
+namespace {
+// Pull the winner's payload from its owner's mapped payload slots (parity of the last step).
+__global__ void bp_pull_payload_kernel(uint8_t* const* peer_base, const int32_t* winner, int b_loc,
+                                       size_t payload_off, size_t payload, int parity, uint4* out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int w = *winner;
+  const int owner = w / b_loc;
+  const uint4* src = reinterpret_cast<const uint4*>(
+      peer_base[owner] + payload_off + ((size_t)parity * b_loc + (w - owner * b_loc)) * payload);
+  const size_t n16 = payload / 16;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = src[i];
+}
+}  // namespace
+
+extern "C" void* lopa_bp_payload_slots(lopa_bp_t* bp, int32_t parity) {
+  if (!bp || !bp->p2p_base || bp->p2p_payload == 0 || parity < 0 || parity > 1) return nullptr;
+  return bp->p2p_base + bp->p2p_payload_off + (size_t)parity * bp->p2p_b_loc * bp->p2p_payload;
+}
+
+extern "C" int lopa_bp_commit_winner_p2p(lopa_bp_t* bp, const int32_t* winner, void* out, void* stream) {
+  if (!bp || !winner || !out || !bp->p2p_open || bp->p2p_payload == 0 || bp->epoch == 0)
+    return LOPA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(out) & 15) return LOPA_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, bp->device);
+  const size_t want = (bp->p2p_payload / 16 + 255) / 256;
+  const int grid = (int)(want < (size_t)(4 * sms) ? (want ? want : 1) : (size_t)(4 * sms));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int parity = (int)(bp->epoch & 1u);
+  return cudaLaunchKernelEx(&cfg, bp_pull_payload_kernel, (uint8_t* const*)bp->d_peer_base, winner,
+                            (int)bp->p2p_b_loc, bp->p2p_payload_off, bp->p2p_payload, parity,
+                            static_cast<uint4*>(out)) == cudaSuccess
+             ? LOPA_OK
+             : LOPA_ERR_CUDA;
 }

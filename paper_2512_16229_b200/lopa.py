@@ -84,7 +84,9 @@ _SIGS = {
     "lopa_bp_create": (_i32, [_c_void_p, _i32, _i32, _i32, ctypes.POINTER(_c_void_p)]),
     "lopa_bp_step": (_i32, [_c_void_p, ctypes.POINTER(StepArgs), _i32, _c_void_p, _c_void_p]),
     "lopa_bp_check": (_i32, [_c_void_p]),
-    "lopa_bp_p2p_alloc": (_i32, [_c_void_p, _i32, _i32, _c_void_p]),
+    "lopa_bp_p2p_alloc": (_i32, [_c_void_p, _i32, _i32, _size, _c_void_p]),
+    "lopa_bp_payload_slots": (_c_void_p, [_c_void_p, _i32]),
+    "lopa_bp_commit_winner_p2p": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_bp_p2p_open": (_i32, [_c_void_p, _c_void_p]),
     "lopa_bp_step_p2p": (_i32, [_c_void_p, ctypes.POINTER(StepArgs), _i32, _c_void_p]),
     "lopa_bp_commit_winner": (_i32, [_c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p, _c_void_p]),
@@ -464,7 +466,8 @@ class BranchParallel:
 
     The NCCL unique id is created by rank 0 and shipped over the given torch process group."""
 
-    def __init__(self, stepper: Stepper, rank: int, world: int, group=None, p2p: bool = False):
+    def __init__(self, stepper: Stepper, rank: int, world: int, group=None, p2p: bool = False,
+                 payload_bytes: int = 0):
         """p2p=True: exchange the records over peer memory (lopa_bp_step_p2p: CUDA IPC mappings
         of every rank's record buffer, NVLink stores + epoch flags) instead of ncclAllGather."""
         import torch.distributed as dist
@@ -493,9 +496,10 @@ class BranchParallel:
         self.argmax = torch.full((self.b_loc, W), -1, dtype=torch.int32, device=d)
         self.scores = torch.empty(world * self.b_loc, dtype=torch.float32, device=d)
         self.p2p = p2p
+        self._payload_bytes = payload_bytes
         if p2p:
             hbuf = (ctypes.c_uint8 * IPC_HANDLE_BYTES)()
-            _check(lib().lopa_bp_p2p_alloc(self.h, W, self.b_loc, hbuf), "lopa_bp_p2p_alloc")
+            _check(lib().lopa_bp_p2p_alloc(self.h, W, self.b_loc, payload_bytes, hbuf), "lopa_bp_p2p_alloc")
             mine = bytes(hbuf)
             if world > 1:
                 allh = [None] * world
@@ -534,6 +538,34 @@ class BranchParallel:
         w = self.s.out.winner if winner is None else winner
         _check(lib().lopa_bp_commit_winner(self.h, _p(w), self.b_loc, _p(flat), nbytes, _p(out),
                                            _stream(flat.device)), "lopa_bp_commit_winner")
+        return out
+
+    def payload_slots(self, parity: int) -> int:
+        """Device pointer of this rank's [b_loc][payload_bytes] payload slots of a parity
+        (peer-memory mode with payload_bytes > 0), 0 if none."""
+        return lib().lopa_bp_payload_slots(self.h, parity) or 0
+
+    def payload_view(self, parity: int) -> torch.Tensor:
+        """The payload slots of a parity as a uint8 tensor [b_loc][payload_bytes] (zero copy,
+        through __cuda_array_interface__); the caller writes step e's payloads into parity
+        e & 1 before that step."""
+        ptr = self.payload_slots(parity)
+        if not ptr:
+            raise LopaError("no payload slots (p2p=True and payload_bytes > 0 needed)")
+        nb = self._payload_bytes
+
+        class _Slots:
+            __cuda_array_interface__ = {"shape": (self.b_loc, nb), "typestr": "|u1", "data": (ptr, False),
+                                        "version": 3, "strides": None}
+
+        return torch.as_tensor(_Slots(), device=self.s.device)
+
+    def commit_winner_p2p(self, out: torch.Tensor, winner: torch.Tensor | None = None) -> torch.Tensor:
+        """NEXT-3 over peer memory: the last step's winner payload pulled from its owner."""
+        _need_cuda(out)
+        w = self.s.out.winner if winner is None else winner
+        _check(lib().lopa_bp_commit_winner_p2p(self.h, _p(w), _p(out), _stream(out.device)),
+               "lopa_bp_commit_winner_p2p")
         return out
 
     def check(self):

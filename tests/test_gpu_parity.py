@@ -448,6 +448,35 @@ def test_bp_p2p_single_rank(L):
         bp.close()
 
 
+def test_bp_commit_winner_p2p_single_rank(L):
+    """NEXT-3 over peer memory with one rank: each step's payloads are written into the slots of
+    the step's parity before the step; afterwards the winner's payload is pulled bit-exactly."""
+    V, W, k, tau, nbytes = 1000, 16, 3, 0.9, 4096
+    st = L.Stepper(V, W, k + 1, k, tau, DEV)
+    bp = L.BranchParallel(st, 0, 1, p2p=True, payload_bytes=nbytes)
+    try:
+        tok, msk, nb = G.fresh_tables(k, W, DEV)
+        logits = torch.zeros((k + 1, W, st.ld), dtype=torch.bfloat16, device=DEV)
+        out = torch.empty(nbytes, dtype=torch.uint8, device=DEV)
+        for e in range(1, 5):
+            pay = torch.randint(0, 256, (bp.b_loc, nbytes), dtype=torch.uint8, device=DEV)
+            bp.payload_view(e & 1).copy_(pay)   # the owner writes step e's payloads (parity e & 1)
+            n = int(nb.item())
+            L.syn_generate(3, 0, V, tok, msk, n_branches=n, out=logits[:n])
+            o = bp.step(logits, nb, tok, msk)
+            bp.commit_winner_p2p(out)
+            torch.cuda.synchronize()
+            assert int(o.status.item()) == 0
+            w = int(o.winner.item())
+            assert torch.equal(out, pay[w])
+            if int(o.n_next.item()) == 0:
+                break
+            tok, msk, nb = o.next_tokens.clone(), o.next_mask.clone(), o.n_next.clone()
+        bp.check()
+    finally:
+        bp.close()
+
+
 @pytest.mark.parametrize("nbytes", [16, 4096, 1835008])
 def test_bp_commit_winner_single_rank(L, nbytes):
     """NEXT-3 Commit-Winner-Cache over the real NCCL path (one rank): the winner's payload
