@@ -372,6 +372,34 @@ class Stepper:
         return self.out
 
 
+def decode_block(forward, tokens0: torch.Tensor, mask0: torch.Tensor, k: int, tau: float, vocab: int,
+                 stepper: "Stepper | None" = None, max_forwards: int | None = None):
+    """Alg. 1 over one window: initial predict, then verify steps until the
+    selected branch has no masked position (R21).  ``forward(branch_tokens[n][W],
+    branch_mask[n][W], out=logits[n][W][ld])`` fills the bf16 logits of the n present branch
+    states (the model).  Returns (tokens int32 [W] on the device, forwards); forwards =
+    1 + verify passes.  One host read per iteration (the branch count)."""
+    W = tokens0.numel()
+    dev = tokens0.device
+    st = stepper or Stepper(vocab, W, k + 1, k, tau, dev)
+    tok = torch.zeros((k + 1, W), dtype=torch.int32, device=dev)
+    msk = torch.zeros((k + 1, W), dtype=torch.uint8, device=dev)
+    tok[0], msk[0] = tokens0.to(torch.int32), _u8(mask0)
+    nb = torch.ones(1, dtype=torch.int32, device=dev)
+    logits = torch.zeros((k + 1, W, st.ld), dtype=torch.bfloat16, device=dev)
+    forwards, n = 0, 1
+    while True:
+        forward(tok[:n], msk[:n], out=logits[:n])
+        out = st.step(logits, nb, tok, msk)
+        forwards += 1
+        n = int(out.n_next.item())
+        if n == 0 or (max_forwards is not None and forwards >= max_forwards):
+            return out.next_tokens[0].clone(), forwards
+        tok.copy_(out.next_tokens)
+        msk.copy_(out.next_mask)
+        nb.copy_(out.n_next)
+
+
 class StepLoopGraph:
     """`iters` Alg. 1 iterations captured in ONE CUDA graph (no tracing compiler, no host
     round trip between steps): each iteration is a lopa_step on logits[i % len(logits)]

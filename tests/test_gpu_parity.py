@@ -321,18 +321,12 @@ def test_step_all_unmasked_block_is_done(L):
 
 # ----------------------------------------------------------------------------- loop
 def _gpu_decode_block(L, seed, V, W, k, tau, extras, blk=0):
-    st = L.Stepper(V, W, k + 1, k, tau, DEV)
-    tok, msk, nb = G.fresh_tables(k, W, DEV)
-    forwards = 0
-    logits = torch.zeros((k + 1, W, st.ld), dtype=torch.bfloat16, device=DEV)
-    while True:
-        n = int(nb.item())
-        L.syn_generate(seed, blk, V, tok, msk, n_branches=n, extras=extras, out=logits[:n])
-        out = st.step(logits, nb, tok, msk)
-        forwards += 1
-        if int(out.n_next.item()) == 0:
-            return out.next_tokens[0].cpu().numpy(), forwards
-        tok, msk, nb = out.next_tokens.clone(), out.next_mask.clone(), out.n_next.clone()
+    """The package's Alg. 1 loop (lopa.decode_block) on the SYN-D2F forward."""
+    fwd = lambda t, m, out: L.syn_generate(seed, blk, V, t, m, extras=extras, out=out)
+    tok0 = torch.zeros(W, dtype=torch.int32, device=DEV)
+    msk0 = torch.ones(W, dtype=torch.uint8, device=DEV)
+    tokens, forwards = L.decode_block(fwd, tok0, msk0, k, tau, V)
+    return tokens.cpu().numpy(), forwards
 
 
 @pytest.mark.parametrize("seed", range(20))
