@@ -36,7 +36,8 @@ if os.path.exists(rep):
     rr = list(csv.reader(io.StringIO(raw)))
     h = rr[0]
     want = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
-            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "dram__bytes_read.sum.pct_of_peak_sustained_elapsed",
+            "sm__cycles_elapsed.avg.per_second", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
             "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
             "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct"]
