@@ -174,6 +174,50 @@ def cpu_baseline_oracle(full, tok, msk, nb, k, tau, budget_s=12.0):
                       f"in {el:.1f} s, NumPy fp64 single thread"}
 
 
+def cpu_baseline_all_cores(full, tok, msk, nb, k, tau, budget_s=8.0):
+    """The same oracle step with its row reductions spread over every host core (threads;
+    NumPy releases the GIL inside the vectorised exp / sum), as SURVEY §8(d) asks next to the
+    one-core figure.  The decisions (O(W k)) stay single-threaded."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import lopa_oracle as O
+    n = int(nb.item())
+    L16 = full.view(torch.int16).cpu().numpy().view(np.uint16)[:n]
+    t_np, m_np = tok.cpu().numpy()[:n], msk.cpu().numpy()[:n]
+    rows = [(j, i) for j in range(n) for i in range(m_np.shape[1]) if m_np[j, i]]
+    cores = len(os.sched_getaffinity(0))
+    shards = [rows[c::cores] for c in range(cores)]
+
+    def reduce_shard(sh):
+        return [(j, i, O.row_confidence(L16[j, i])) for (j, i) in sh]
+
+    reps, t0 = 0, time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        while True:
+            conf = np.full(m_np.shape, np.nan)
+            amax = np.full(m_np.shape, -1, dtype=np.int64)
+            for part in ex.map(reduce_shard, shards):
+                for (j, i, (c, a, _)) in part:
+                    conf[j, i], amax[j, i] = c, a
+            scores = [O.branch_score(conf[j], m_np[j]) for j in range(n)]
+            w = O.verify_select(scores)
+            anc = O.anchor_fill(conf[w], amax[w], t_np[w], m_np[w], tau)
+            O.spawn_branches(conf[w], amax[w], anc.tokens, anc.mask, k)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s:
+                break
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"value": reps / el, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": model,
+            "sample": f"{reps} full verify steps, row reductions over {cores} threads, in {el:.1f} s"}
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
@@ -384,6 +428,46 @@ def run_lopa(args):
         bp.check()
     value = K / (el_ms / 1000.0)
     pair_ms = statistics.mean(per) if per else float("nan")
+    # step-time distribution: the same steps in 20 batches, CUDA events at the
+    # batch ends only; per-batch mean step time -> p10 / p50 / p90
+    nbatch = 20
+    per_b = max(1, K // nbatch)
+    bt = []
+    head_start(stream)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(nbatch + 1)]
+    evs[0].record(stream)
+    for b_ in range(nbatch):
+        for i in range(b_ * per_b, (b_ + 1) * per_b):
+            launch(i)
+        evs[b_ + 1].record(stream)
+    torch.cuda.synchronize()
+    bt = sorted(evs[b_].elapsed_time(evs[b_ + 1]) * 1000.0 / per_b for b_ in range(nbatch))
+    step_dist = {"p10_us": bt[1], "p50_us": bt[nbatch // 2], "p90_us": bt[-2], "batches": nbatch,
+                 "steps_per_batch": per_b}
+    # dense kernel roofline (SURVEY §8(d) mode (i)): every (branch, position) row of the
+    # buffers reduced, (k + 1) * W rows, same CUDA-event chain as pass A
+    dense = None
+    if bp is None:
+        dmask = torch.ones(n_rows, dtype=torch.uint8, device=dev)
+
+        def dense_call(i):
+            s_ = L.lopa_confidence(P_(bufs[i % n_buf]), ldv, n_rows, V, P_(dmask), P_(c_out), P_(a_out),
+                                   P_(c_st), P_(c_ws), c_ws.numel(), sptr)
+            if s_:
+                raise lopa.LopaError(f"lopa_confidence status {s_}")
+
+        for i in range(args.warmup):
+            dense_call(i)
+        torch.cuda.synchronize()
+        head_start(stream)
+        c0.record(stream)
+        for i in range(K):
+            dense_call(i)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        d_ms = c0.elapsed_time(c1) / K
+        d_bytes = 2.0 * V * n_rows
+        dense = {"rows": n_rows, "kernel_ms_mean": d_ms, "achieved_gbs": d_bytes / (d_ms / 1000.0) / 1e9}
     kern_ms = chain_ms
     alg_bytes = 2.0 * V * rows_local                 # 2 B per logit of a masked row
     achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
@@ -449,9 +533,10 @@ def run_lopa(args):
                "d2h_bytes_per_step": d2h, "steps": K2}
 
     if rank == 0:
-        cpu = None
+        cpu = cpu_all = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline_oracle(full, tok, msk, nb, k, tau)
+            cpu_all = cpu_baseline_all_cores(full, tok, msk, nb, k, tau)
         traffic = None
         tf = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tf):
@@ -471,6 +556,7 @@ def run_lopa(args):
                        "l2": f"rotating {n_buf} logits buffers ({n_buf * full.numel() * 2 / 1e6:.0f} MB >= 4x L2)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "frac_datasheet_8tbs": achieved / 8000.0,
                          "kernel": "lopa_reduce_kernel (K1, a1 vocabulary reduction)",
                          "kernel_ms_mean": kern_ms,
                          "kernel_timing": f"CUDA events around {K} back-to-back lopa_confidence calls (K1 + its 1-CTA fold kernel, PDL-chained as in lopa_step) over this rank's {rows_local} masked rows: an upper bound of K1's in-step duration",
@@ -486,8 +572,14 @@ def run_lopa(args):
             line["e2e"] = e2e
         if graph_loop is not None:
             line["graph_loop"] = graph_loop
+        line["step_time_distribution"] = step_dist
+        if dense is not None:
+            dense["frac"] = dense["achieved_gbs"] / peak
+            line["dense_roofline"] = dense
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if cpu_all is not None:
+            line["cpu_baseline_all_cores"] = cpu_all
         print(json.dumps(line), flush=True)
     if bp is not None:
         bp.close()
