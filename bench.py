@@ -496,6 +496,27 @@ def run_lopa(args):
                       "replays": reps, "note": "one CUDA graph per 32-iteration loop (tables fed back on "
                       "the device; fixed logits buffers, so later iterations have fewer masked rows)"}
 
+    # the Alg. 1 loop over whole blocks (SURVEY §8(d) "TPF, loop only"): lopa.decode_block on the
+    # SYN-D2F forward (generator + step per iteration, device time), 8 blocks of this shape
+    loop = None
+    if world == 1 and bp is None:
+        fw_total, tok_total = 0, 0
+        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st_l = lopa.Stepper(V, W, k + 1, k, tau, dev)
+        l0.record(stream)
+        for blk in range(8):
+            fwd = lambda t, m, out, blk=blk: lopa.syn_generate(seed, blk, V, t, m, out=out)
+            t0_ = torch.zeros(W, dtype=torch.int32, device=dev)
+            m0_ = torch.ones(W, dtype=torch.uint8, device=dev)
+            _, fw = lopa.decode_block(fwd, t0_, m0_, k, tau, V, stepper=st_l)
+            fw_total += fw
+            tok_total += W
+        l1.record(stream)
+        torch.cuda.synchronize()
+        loop = {"blocks": 8, "tokens": tok_total, "forwards": fw_total, "tpf": tok_total / fw_total,
+                "ms_per_block_incl_generator": l0.elapsed_time(l1) / 8,
+                "note": "one host read per iteration (branch count); SYN-D2F forward on the GPU"}
+
     # e2e through the public API with HOST buffers: pinned logits -> device, step, results -> host
     e2e = None
     if world == 1:
@@ -573,6 +594,8 @@ def run_lopa(args):
         if graph_loop is not None:
             line["graph_loop"] = graph_loop
         line["step_time_distribution"] = step_dist
+        if loop is not None:
+            line["decode_loop"] = loop
         if dense is not None:
             dense["frac"] = dense["achieved_gbs"] / peak
             line["dense_roofline"] = dense
