@@ -496,6 +496,25 @@ def run_lopa(args):
                       "replays": reps, "note": "one CUDA graph per 32-iteration loop (tables fed back on "
                       "the device; fixed logits buffers, so later iterations have fewer masked rows)"}
 
+    # BP: the exchange's collective alone (SURVEY §8(d) "comm µs"): the same all-gather size
+    # through the torch NCCL process group, CUDA events around 200 back-to-back calls
+    comm = None
+    if bp is not None and dist is not None:
+        sendb = torch.zeros(bp.rb, dtype=torch.uint8, device=dev)
+        recvb = torch.empty(world * bp.rb, dtype=torch.uint8, device=dev)
+        for _ in range(10):
+            dist.all_gather_into_tensor(recvb, sendb)
+        torch.cuda.synchronize()
+        dist.barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for _ in range(200):
+            dist.all_gather_into_tensor(recvb, sendb)
+        x1.record(stream)
+        torch.cuda.synchronize()
+        comm = {"allgather_us": x0.elapsed_time(x1) * 1000.0 / 200, "bytes_per_rank": bp.rb,
+                "note": "torch all_gather_into_tensor of the record size (the exchange's collective)"}
+
     # the Alg. 1 loop over whole blocks (SURVEY §8(d) "TPF, loop only"): lopa.decode_block on the
     # SYN-D2F forward (generator + step per iteration, device time), 8 blocks of this shape
     loop = None
@@ -596,6 +615,8 @@ def run_lopa(args):
         line["step_time_distribution"] = step_dist
         if loop is not None:
             line["decode_loop"] = loop
+        if comm is not None:
+            line["bp_comm"] = comm
         if dense is not None:
             dense["frac"] = dense["achieved_gbs"] / peak
             line["dense_roofline"] = dense
