@@ -7,7 +7,8 @@
 //     <= 32 KB into a kStages-deep ring, mbarrier transaction bytes, L2 evict-first.  Items are
 //     numbered group-major so the short last group of every row streams at the very end.
 //   * CTA b takes items b and G + b (the first one issued before the row masks arrive), then
-//     claims items from a global counter, two claims in flight; unmasked rows are skipped.
+//     claims items from a global counter, two claims in flight (the first two sent before the
+//     masks arrive); unmasked rows are skipped.
 //   * kConsumerWGs consumer warpgroups share the stages (warpgroup w: segment w % 2 of the
 //     stages of phase w / 2); each warp reduces an interleaved quarter of its segment with
 //     128-bit shared loads: exact max (max.NaN.bf16x2), sum of exp2((x - m) log2 e) with x - m
@@ -22,7 +23,8 @@
 //   top-k spawn (MODE_STEP / MODE_DECIDE) or the branch-parallel record (MODE_BP_LOCAL).
 //
 // Compile-time knobs (A/B builds via build.py --variant; defaults are the measured best):
-//   LOPA_STAGES, LOPA_WGS, LOPA_CTAS_PER_SM, LOPA_CLAIM_AHEAD, LOPA_SEG_ELEMS,
+//   LOPA_STAGES, LOPA_WGS, LOPA_CTAS_PER_SM, LOPA_CLAIM_AHEAD, LOPA_SPEC_ITEMS,
+//   LOPA_EARLY_CLAIMS, LOPA_SEG_ELEMS,
 //   LOPA_SEG_PER_ITEM, LOPA_MBAR_SUSPEND_NS, LOPA_TAIL_THREADS, LOPA_POLY_WORDS (exp2 on the FMA
 //   pipe), LOPA_LATE_ARGMAX; experiments only: LOPA_NOCOMPUTE (streaming without arithmetic),
 //   LOPA_EXP_NOARGMAX, LOPA_NO_PDL, LOPA_NO_TLB_WARM; LOPA_TIMELINE (per-CTA %globaltimer
@@ -90,6 +92,14 @@ namespace lopa {
 #endif
 #ifndef LOPA_CTAS_PER_SM
 #define LOPA_CTAS_PER_SM 1
+#endif
+// statically assigned work items issued before the row masks arrive (1..kStages), and whether
+// the first two dynamic claims are issued at the same time
+#ifndef LOPA_SPEC_ITEMS
+#define LOPA_SPEC_ITEMS 1
+#endif
+#ifndef LOPA_EARLY_CLAIMS
+#define LOPA_EARLY_CLAIMS 1
 #endif
 constexpr int kStages = LOPA_STAGES;      // TMA ring depth (one <= 32 KB work item per stage)
 constexpr int kConsumerWGs = LOPA_WGS;    // consumer warpgroups per CTA
@@ -686,9 +696,24 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     ++i;
   };
   const int b = blockIdx.x;
+  // items q G + b (q < kStatic) are assigned statically; the first kSpec of them are issued
+  // before the row masks arrive (speculative: validity is checked by the consumers)
+  constexpr int kSpec = LOPA_SPEC_ITEMS < kStages ? LOPA_SPEC_ITEMS : kStages;
+  constexpr int kStatic = kSpec > 2 ? kSpec : 2;
+  const bool dyn = kStatic * G < n_items_cap;
+  uint32_t p1 = 0x7FFFFFFFu, p2 = 0x7FFFFFFFu;
   if (tid == 0) {
     TL(1);
-    if (b < n_items_cap) issue(b);  // speculative: validity is checked by the consumers
+#pragma unroll
+    for (int q = 0; q < kSpec; ++q)
+      if (q * G + b < n_items_cap) issue(q * G + b);
+#if LOPA_EARLY_CLAIMS && LOPA_CLAIM_AHEAD == 2
+    // the first two claims travel while the masks load
+    if (dyn) {
+      p1 = atomicAdd(&P.ctrs[0], 1u);
+      p2 = atomicAdd(&P.ctrs[0], 1u);
+    }
+#endif
   }
   // valid-row bits: mask byte and n_branches loaded independently (one round trip)
   const int n_groups = (P.n_cand + 31) >> 5;
@@ -711,32 +736,37 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
       // ---- TMA producer: items b (issued above), G + b, then 2G + counter, ...  Claims on
       // unmasked rows are skipped without a copy; two claims stay in flight so the atomic's
       // latency hides behind the issue of two items.
-      const bool dyn = 2 * G < n_items;
       auto maybe_issue = [&](int cur) {
         if (row_valid(cur % P.n_cand)) issue(cur);
       };
 #if LOPA_CLAIM_AHEAD == 2
-      uint32_t p1 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
-      uint32_t p2 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
-      if (G + b < n_items) maybe_issue(G + b);
+#if !LOPA_EARLY_CLAIMS
+      if (dyn) {
+        p1 = atomicAdd(&P.ctrs[0], 1u);
+        p2 = atomicAdd(&P.ctrs[0], 1u);
+      }
+#endif
+      for (int q = kSpec; q < kStatic; ++q)
+        if (q * G + b < n_items) maybe_issue(q * G + b);
       if (dyn) {
         while (true) {
-          const int c1 = 2 * G + (int)p1;
+          const int c1 = kStatic * G + (int)p1;
           if (c1 >= n_items) break;
           p1 = atomicAdd(&P.ctrs[0], 1u);
           maybe_issue(c1);
-          const int c2 = 2 * G + (int)p2;
+          const int c2 = kStatic * G + (int)p2;
           if (c2 >= n_items) break;
           p2 = atomicAdd(&P.ctrs[0], 1u);
           maybe_issue(c2);
         }
       }
 #elif LOPA_CLAIM_AHEAD == 1
-      uint32_t p1 = dyn ? atomicAdd(&P.ctrs[0], 1u) : 0x7FFFFFFFu;
-      if (G + b < n_items) maybe_issue(G + b);
+      if (dyn) p1 = atomicAdd(&P.ctrs[0], 1u);
+      for (int q = kSpec; q < kStatic; ++q)
+        if (q * G + b < n_items) maybe_issue(q * G + b);
       if (dyn) {
         while (true) {
-          const int c1 = 2 * G + (int)p1;
+          const int c1 = kStatic * G + (int)p1;
           if (c1 >= n_items) break;
           p1 = atomicAdd(&P.ctrs[0], 1u);
           maybe_issue(c1);
@@ -744,11 +774,12 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
       }
 #else
       // claim only once a stage is free: no item is committed to this CTA before it can start
-      if (G + b < n_items) maybe_issue(G + b);
+      for (int q = kSpec; q < kStatic; ++q)
+        if (q * G + b < n_items) maybe_issue(q * G + b);
       if (dyn) {
         while (true) {
           if (i >= (uint32_t)kStages) mbar_wait(&empty[i % kStages], ((i / kStages) - 1) & 1);
-          const int c = 2 * G + (int)atomicAdd(&P.ctrs[0], 1u);
+          const int c = kStatic * G + (int)atomicAdd(&P.ctrs[0], 1u);
           if (c >= n_items) break;
           maybe_issue(c);
         }

@@ -149,6 +149,23 @@ __device__ __forceinline__ void cta_range(int b, int G, int n_units, int* u0, in
   *u1 = (int)(((long long)(b + 1) * n_units) / G);
 }
 
+// Tile t of a CTA's n_units units (default: 256-column tiles and one narrow remainder).  With
+// LOPA_LMH_BALANCED (measured +9 us on the Dream LM head, rejected) the ceil(n_units / 16) tiles get
+// near-equal widths (65 units -> 5 x 13, i.e. 208 columns each) instead of full 256-column tiles
+// plus one narrow remainder tile whose hidden-state reloads dominate its time.
+#ifndef LOPA_LMH_BALANCED
+#define LOPA_LMH_BALANCED 0
+#endif
+__device__ __forceinline__ void tile_cols(int u0, int n_units, int n_tiles, int t, int* v0, int* N) {
+#if LOPA_LMH_BALANCED
+  const int a = (t * n_units) / n_tiles, e = ((t + 1) * n_units) / n_tiles;
+#else
+  const int a = 16 * t, e = min(n_units, 16 * t + 16);
+#endif
+  *v0 = (u0 + a) * 16;
+  *N = (e - a) * 16;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     lopa_lmhead_kernel(const __grid_constant__ CUtensorMap map_a,
                        const __grid_constant__ CUtensorMap map_b256,
@@ -204,8 +221,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
       uint32_t it = 0;
       for (int t = 0; t < n_tiles; ++t) {
-        const int v0 = (u0 + 16 * t) * 16;
-        const int N = min(16, u1 - u0 - 16 * t) * 16;
+        int v0, N;
+        tile_cols(u0, u1 - u0, n_tiles, t, &v0, &N);
         const uint32_t bytes = (uint32_t)(n_half * kHalfBytes + N * kBK * 2);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = (int)(it % kStages);
@@ -232,7 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- MMA issuer
     uint32_t it = 0;
     for (int t = 0; t < n_tiles; ++t) {
-      const int N = min(16, u1 - u0 - 16 * t) * 16;
+      int v0_unused, N;
+      tile_cols(u0, u1 - u0, n_tiles, t, &v0_unused, &N);
       const int a = t % n_acc;
       {
         LMH_T0();
@@ -281,8 +299,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m = -INFINITY, ssum = 0.f;
     int am = 0x7FFFFFFF;
     for (int t = 0; t < n_tiles; ++t) {
-      const int v0 = (u0 + 16 * t) * 16;
-      const int N = min(16, u1 - u0 - 16 * t) * 16;
+      int v0, N;
+      tile_cols(u0, u1 - u0, n_tiles, t, &v0, &N);
       const int a = t % n_acc;
       {
         LMH_T0();
