@@ -411,6 +411,25 @@ def run_lopa(args):
     chain_ms = c0.elapsed_time(c1) / K
     if int(c_st.item()) != 0:
         raise lopa.LopaError(f"device status {int(c_st.item())}")
+
+    # K1 alone (lopa_debug_reduce_only: the step's launch configuration, no fold kernel),
+    # K back-to-back PDL-chained launches over the same rows: K1's average launch duration
+    def k1_call(i):
+        s_ = L.lopa_debug_reduce_only(P_(bufs[i % n_buf]), ldv, n_rows, V, P_(rmask), P_(c_st),
+                                      P_(c_ws), c_ws.numel(), sptr)
+        if s_:
+            raise lopa.LopaError(f"lopa_debug_reduce_only status {s_}")
+
+    for i in range(args.warmup):
+        k1_call(i)
+    torch.cuda.synchronize()
+    head_start(stream)
+    c0.record(stream)
+    for i in range(K):
+        k1_call(i)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    k1_ms = c0.elapsed_time(c1) / K
     # roofline pass B (context): an event pair around every K1 inside the same K steps; each
     # pair also holds K1's launch latency, which the step's PDL chain otherwise hides
     # (in batches, each behind a device-side head start, so that host launch overhead never
@@ -451,10 +470,10 @@ def run_lopa(args):
         dmask = torch.ones(n_rows, dtype=torch.uint8, device=dev)
 
         def dense_call(i):
-            s_ = L.lopa_confidence(P_(bufs[i % n_buf]), ldv, n_rows, V, P_(dmask), P_(c_out), P_(a_out),
-                                   P_(c_st), P_(c_ws), c_ws.numel(), sptr)
+            s_ = L.lopa_debug_reduce_only(P_(bufs[i % n_buf]), ldv, n_rows, V, P_(dmask), P_(c_st),
+                                          P_(c_ws), c_ws.numel(), sptr)
             if s_:
-                raise lopa.LopaError(f"lopa_confidence status {s_}")
+                raise lopa.LopaError(f"lopa_debug_reduce_only status {s_}")
 
         for i in range(args.warmup):
             dense_call(i)
@@ -468,7 +487,7 @@ def run_lopa(args):
         d_ms = c0.elapsed_time(c1) / K
         d_bytes = 2.0 * V * n_rows
         dense = {"rows": n_rows, "kernel_ms_mean": d_ms, "achieved_gbs": d_bytes / (d_ms / 1000.0) / 1e9}
-    kern_ms = chain_ms
+    kern_ms = k1_ms
     alg_bytes = 2.0 * V * rows_local                 # 2 B per logit of a masked row
     achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
     pk = peaks()
@@ -599,7 +618,9 @@ def run_lopa(args):
                          "frac_datasheet_8tbs": achieved / 8000.0,
                          "kernel": "lopa_reduce_kernel (K1, a1 vocabulary reduction)",
                          "kernel_ms_mean": kern_ms,
-                         "kernel_timing": f"CUDA events around {K} back-to-back lopa_confidence calls (K1 + its 1-CTA fold kernel, PDL-chained as in lopa_step) over this rank's {rows_local} masked rows: an upper bound of K1's in-step duration",
+                         "kernel_timing": f"CUDA events around {K} back-to-back K1 launches (lopa_debug_reduce_only: the step's grid, PDL-chained as in lopa_step, each waiting for the previous to complete) over this rank's {rows_local} masked rows of the rotating buffers",
+                         "conf_call_ms": chain_ms,
+                         "conf_call_note": "the same rows through lopa_confidence (K1 + its 1-CTA fold kernel), back to back",
                          "k1_event_pair_ms": pair_ms,
                          "k1_event_pair_note": "event pair around each K1 inside lopa_step; includes K1's launch latency that PDL hides in the timed steps",
                          "alg_bytes_per_launch": alg_bytes,

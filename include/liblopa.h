@@ -246,6 +246,15 @@ void lopa_bp_destroy(lopa_bp_t* bp);
 int lopa_profile_enable(int32_t max_records);
 int lopa_profile_read(float* k1_ms, int32_t max, int32_t* n_out);
 
+/* Measurement: K1 (the vocabulary-reduction kernel) alone, as launched inside lopa_step (one
+ * CTA per SM but one), over the rows of a lopa_confidence call: it leaves only the per-group
+ * partials in the workspace (no conf / argmax).  Lets bench.py time K1's average launch
+ * duration with CUDA events around back-to-back launches.  Arguments and errors as
+ * lopa_confidence. */
+int lopa_debug_reduce_only(const void* logits_bf16, int64_t ld, int32_t n_rows, int32_t vocab,
+                           const uint8_t* row_mask, int32_t* dev_status, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* Debug: per-CTA phase timeline (%globaltimer ns) of the last reduction launch, for builds
  * compiled with -DLOPA_TIMELINE; returns the slots per CTA written to out[n_ctas][slots], or 0.
  * Slots: 0 CTA start, 1 producer start, 2 first stage consumed, 3 last unit consumed,

@@ -131,7 +131,7 @@ struct Params {
   float* conf;
   int32_t* argmax;
   int32_t* dev_status;
-  uint32_t* ctrs;              // [0] work-item counter
+  uint32_t* ctrs;              // [0] work-item counter, [1] producers done (K1 self-reset)
   float4* gpart;               // [n_grp][n_cand] group partials (m, s, argmax bits, -), group-major
   int mode;
   // tails
@@ -785,6 +785,16 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
         }
       }
 #endif
+      // Self-reset of the work counter: every producer, once done claiming (its outstanding
+      // claims returned), takes a ticket; the last one zeroes the counter and the tickets, so a
+      // launch leaves the workspace zeroed without any follow-up kernel.
+      asm volatile("" ::"r"(p1), "r"(p2));
+      __threadfence();
+      if (atomicAdd(&P.ctrs[1], 1u) == (uint32_t)G - 1) {
+        __threadfence();
+        P.ctrs[0] = 0;
+        P.ctrs[1] = 0;
+      }
       // end-of-work sentinels: one stage per consumer phase (every warpgroup sees one)
       for (int c = 0; c < kWgStride; ++c, ++i) {
         const int s = (int)(i % kStages);
@@ -1054,7 +1064,6 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   if (MODE == MODE_STEP || MODE == MODE_DECIDE) cta_tail_step<kTailThreads, S>(P, T, tid, nb);
   if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads, S>(P, T, tid, nb);
   if (tid == 0) {
-    P.ctrs[0] = 0;
     TL(5);
     TLC(20);
   }
@@ -1109,7 +1118,6 @@ __global__ void __launch_bounds__(kFoldRows) lopa_fold_kernel(const Params P) {
     P.argmax[r] = (int32_t)f.a;
     if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrs[0] = 0;
 }
 
 static_assert(kTailThreads >= LOPA_MAX_WINDOW, "one tail thread per window position");
@@ -1399,9 +1407,13 @@ static void prof_record(int which, cudaStream_t s, int* slot) {
 
 // K1 (streaming reduction) then K2 (fold + decisions, or the fold only for MODE_CONF), both
 // with programmatic dependent launch so launch latency overlaps the previous kernel.
-static int launch_reduce(const Params& P, int device, cudaStream_t s) {
+static int launch_reduce(const Params& P, int device, cudaStream_t s, bool k1_only = false) {
   int st = ensure_kernel_attrs(device);
   if (st != LOPA_OK) return st;
+  if (k1_only) {  // measurement: K1 alone, in the step's launch configuration
+    const int g = LOPA_CTAS_PER_SM * (num_sms(device) - 1);
+    return cuda_status(launch_pdl(lopa_reduce_kernel, dim3(g), dim3(kThreads), kSmemBytes, s, P));
+  }
   // One SM is left to the fold/tail kernel: it becomes resident there while K1 streams (PDL)
   // and, landing on the same SM step after step, runs with a warm instruction cache.
   const int grid = LOPA_CTAS_PER_SM * (num_sms(device) - (P.mode == MODE_CONF ? 0 : 1));
@@ -1646,10 +1658,32 @@ extern "C" int32_t lopa_num_segments(int32_t vocab) {
   return ns;
 }
 
+static int confidence_impl(const void* logits, int64_t ld, int32_t n_rows, int32_t vocab,
+                           const uint8_t* row_mask, float* conf, int32_t* argmax,
+                           int32_t* dev_status, void* workspace, size_t workspace_bytes,
+                           void* stream, bool k1_only);
+
 extern "C" int lopa_confidence(const void* logits, int64_t ld, int32_t n_rows, int32_t vocab,
                                const uint8_t* row_mask, float* conf, int32_t* argmax,
                                int32_t* dev_status, void* workspace, size_t workspace_bytes,
                                void* stream) {
+  return confidence_impl(logits, ld, n_rows, vocab, row_mask, conf, argmax, dev_status, workspace,
+                         workspace_bytes, stream, false);
+}
+
+extern "C" int lopa_debug_reduce_only(const void* logits, int64_t ld, int32_t n_rows,
+                                      int32_t vocab, const uint8_t* row_mask, int32_t* dev_status,
+                                      void* workspace, size_t workspace_bytes, void* stream) {
+  static float dummy_conf;
+  static int32_t dummy_argmax;
+  return confidence_impl(logits, ld, n_rows, vocab, row_mask, &dummy_conf, &dummy_argmax,
+                         dev_status, workspace, workspace_bytes, stream, true);
+}
+
+static int confidence_impl(const void* logits, int64_t ld, int32_t n_rows, int32_t vocab,
+                           const uint8_t* row_mask, float* conf, int32_t* argmax,
+                           int32_t* dev_status, void* workspace, size_t workspace_bytes,
+                           void* stream, bool k1_only) {
   if (n_rows < 0) return LOPA_ERR_INVALID_ARG;
   if (!logits_ok(logits, ld, vocab) || !conf || !argmax || !dev_status || !workspace)
     return LOPA_ERR_INVALID_ARG;
@@ -1676,7 +1710,7 @@ extern "C" int lopa_confidence(const void* logits, int64_t ld, int32_t n_rows, i
   P.ctrs = ws.ctrs;
   P.gpart = ws.gpart;
   P.mode = MODE_CONF;
-  return launch_reduce(P, dev, s);
+  return launch_reduce(P, dev, s, k1_only);
 }
 
 extern "C" int lopa_anchor_fill_ex(const float* conf, const int32_t* argmax, const int32_t* tokens,

@@ -66,6 +66,8 @@ _SIGS = {
     "lopa_num_segments": (_i32, [_i32]),
     "lopa_confidence": (_i32, [_c_void_p, _i64, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
                                _c_void_p, _c_void_p, _size, _c_void_p]),
+    "lopa_debug_reduce_only": (_i32, [_c_void_p, _i64, _i32, _i32, _c_void_p, _c_void_p,
+                                      _c_void_p, _size, _c_void_p]),
     "lopa_anchor_fill": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _f32,
                                 _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_anchor_fill_ex": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _f32, _c_void_p,

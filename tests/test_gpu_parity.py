@@ -69,6 +69,37 @@ def test_confidence_rows(L, V):
     assert np.array_equal(amax.cpu().numpy(), ra)
 
 
+@pytest.mark.parametrize("n_rows,V", [(3, 1000), (300, 151936), (40, 8193)])
+def test_reduce_only_leaves_workspace_zeroed(L, n_rows, V):
+    """K1 alone (lopa_debug_reduce_only, bench.py's roofline launches) resets its own work
+    counter: after several back-to-back K1-only launches the workspace counters are zero and a
+    lopa_confidence call on the same workspace is still exact."""
+    rng = np.random.default_rng(n_rows)
+    ld = ((V + 7) // 8) * 8
+    rows = _bits(rng.normal(0, 2, size=(n_rows, V)).astype(np.float32))
+    buf = np.zeros((n_rows, ld), np.uint16)
+    buf[:, :V] = rows
+    t = torch.from_numpy(buf.view(np.int16)).to(DEV).view(torch.bfloat16)
+    rm = torch.from_numpy((rng.random(n_rows) < 0.8).astype(np.uint8)).to(DEV)
+    ws = L.new_workspace(n_rows, V, DEV)
+    st = L.new_status(DEV)
+    import ctypes
+    sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for _ in range(5):
+        assert L.lib().lopa_debug_reduce_only(L._p(t), ld, n_rows, V, L._p(rm), L._p(st), L._p(ws),
+                                              ws.numel(), sp) == 0
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert ws[:8].view(torch.int32).cpu().tolist() == [0, 0]
+    conf, amax, st2 = L.confidence(t, vocab=V, row_mask=rm, workspace=ws)
+    rc, ra, _ = O.confidence(rows)
+    sel = rm.cpu().numpy().astype(bool)
+    assert int(st2.item()) == 0
+    assert np.max(np.abs(conf.cpu().numpy().astype(np.float64)[sel] - rc[sel])) <= G.CONF_TOL
+    assert np.array_equal(amax.cpu().numpy()[sel], ra[sel])
+    assert ws[:8].view(torch.int32).cpu().tolist() == [0, 0]
+
+
 @pytest.mark.parametrize("V", [(1 << 20) + 3, 1 << 23])
 def test_confidence_huge_vocab(L, V):
     """Up to LOPA_MAX_VOCAB = 2^23: 512 groups per row, so the fold takes its sequential
