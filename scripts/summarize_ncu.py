@@ -19,16 +19,32 @@ for r in rows:
 with open(os.path.join(pr, f"{tag}_launches.csv"), "w") as f:
     f.write("id,kernel,gpu__time_duration_ns\n")
     for i, k, v in launches: f.write(f'{i},"{k}",{v:.0f}\n')
-lk = [v for _, k, v in launches if "lopa_reduce" in k][-20:]
-tk = [v for _, k, v in launches if "lopa_tail" in k][-20:]
+# bench.py's timed regions each start behind a spin kernel (head_start): region 1 = the headline
+# steps (K1 + K2 pairs), region 2 = the lopa_confidence chain, region 3 = K1 alone (roofline)
+regions, cur = [], None
+for _, k, v in launches:
+    if "spin_kernel" in k:
+        cur = []
+        regions.append(cur)
+    elif cur is not None:
+        cur.append((k, v))
+def _mean(xs):
+    return sum(xs) / len(xs) if xs else float("nan")
+steps = regions[0][:40] if regions else []
+lk = [v for k, v in steps if "lopa_reduce" in k]
+tk = [v for k, v in steps if "lopa_tail" in k]
+k1_alone = [v for k, v in (regions[2] if len(regions) > 2 else []) if "lopa_reduce" in k][:20]
 out.append(f"# ncu summary ({tag})\n")
 out.append("Command: `python bench.py --steps 20 --warmup 3 --no-cpu-baseline` (Dream verify step, 241 masked rows x V=151936).\n")
 out.append("## Launch list (gpu__time_duration.sum, --clock-control none; serialised, cold-cache)\n")
 if lk and tk:
     mk, mt = sum(lk) / len(lk), sum(tk) / len(tk)
-    out.append(f"- K1 lopa_reduce_kernel: mean {mk/1000:.2f} us over the last {len(lk)} launches")
+    out.append(f"- timed steps (first region): K1 lopa_reduce_kernel mean {mk/1000:.2f} us over {len(lk)} launches")
     out.append(f"- K2 lopa_tail_kernel: mean {mt/1000:.2f} us")
-    out.append(f"- K1 share of the step (K1/(K1+K2)): {mk/(mk+mt):.1%}\n")
+    out.append(f"- K1 share of the step (K1/(K1+K2)): {mk/(mk+mt):.1%}")
+    if k1_alone:
+        out.append(f"- K1 alone (the roofline region, lopa_debug_reduce_only): mean {_mean(k1_alone)/1000:.2f} us over {len(k1_alone)} launches")
+    out.append("")
 rep = os.path.join(go, "prof_full.ncu-rep")
 traffic = None
 if os.path.exists(rep):
