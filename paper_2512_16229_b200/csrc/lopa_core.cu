@@ -6,9 +6,10 @@
 //     into groups of kSegPerItem = 2; a work item is one (group, row) = ONE cp.async.bulk of
 //     <= 32 KB into a kStages-deep ring, mbarrier transaction bytes, L2 evict-first.  Items are
 //     numbered group-major so the short last group of every row streams at the very end.
-//   * CTA b takes items b and G + b (the first one issued before the row masks arrive), then
-//     claims items from a global counter, two claims in flight (the first two sent before the
-//     masks arrive); unmasked rows are skipped.
+//   * CTA b issues its first item (group 0 of row b) before the row masks arrive, then works
+//     over items numbered on the valid (masked, present) rows only: item b, then claims from a
+//     global counter, two claims in flight (the first two sent before the masks arrive).  K1
+//     resets the counter itself (the last producer done claiming zeroes it).
 //   * kConsumerWGs consumer warpgroups share the stages (warpgroup w: segment w % 2 of the
 //     stages of phase w / 2); each warp reduces an interleaved quarter of its segment with
 //     128-bit shared loads: exact max (max.NaN.bf16x2), sum of exp2((x - m) log2 e) with x - m
@@ -23,8 +24,8 @@
 //   top-k spawn (MODE_STEP / MODE_DECIDE) or the branch-parallel record (MODE_BP_LOCAL).
 //
 // Compile-time knobs (A/B builds via build.py --variant; defaults are the measured best):
-//   LOPA_STAGES, LOPA_WGS, LOPA_CTAS_PER_SM, LOPA_CLAIM_AHEAD, LOPA_SPEC_ITEMS,
-//   LOPA_EARLY_CLAIMS, LOPA_SEG_ELEMS,
+//   LOPA_STAGES, LOPA_WGS, LOPA_CTAS_PER_SM, LOPA_NO_COMPACT (raw item numbering only),
+//   LOPA_SEG_ELEMS,
 //   LOPA_SEG_PER_ITEM, LOPA_MBAR_SUSPEND_NS, LOPA_TAIL_THREADS, LOPA_POLY_WORDS (exp2 on the FMA
 //   pipe), LOPA_LATE_ARGMAX; experiments only: LOPA_NOCOMPUTE (streaming without arithmetic),
 //   LOPA_EXP_NOARGMAX, LOPA_NO_PDL, LOPA_NO_TLB_WARM; LOPA_TIMELINE (per-CTA %globaltimer
@@ -83,30 +84,24 @@ namespace lopa {
 #ifndef LOPA_STAGES
 #define LOPA_STAGES 3
 #endif
-// dynamic work claims the producer keeps ahead of its issued items (0, 1 or 2)
-#ifndef LOPA_CLAIM_AHEAD
-#define LOPA_CLAIM_AHEAD 2
-#endif
 #ifndef LOPA_WGS
 #define LOPA_WGS 6
 #endif
 #ifndef LOPA_CTAS_PER_SM
 #define LOPA_CTAS_PER_SM 1
 #endif
-// statically assigned work items issued before the row masks arrive (1..kStages), and whether
-// the first two dynamic claims are issued at the same time
-#ifndef LOPA_SPEC_ITEMS
-#define LOPA_SPEC_ITEMS 1
-#endif
-#ifndef LOPA_EARLY_CLAIMS
-#define LOPA_EARLY_CLAIMS 1
-#endif
+
 constexpr int kStages = LOPA_STAGES;      // TMA ring depth (one <= 32 KB work item per stage)
 constexpr int kConsumerWGs = LOPA_WGS;    // consumer warpgroups per CTA
 constexpr int kThreads = 32 + 128 * kConsumerWGs;
 constexpr int kWarps = kThreads / 32;
 constexpr int kStageBytes = kSegPerItem * 2 * kSegElems;  // one work item per stage
 constexpr int kMaxGroups = LOPA_MAX_ROWS / 32;
+#ifdef LOPA_NO_VLIST_SMEM
+constexpr int kVlistBytes = 0;
+#else
+constexpr int kVlistBytes = LOPA_MAX_ROWS * 2;  // K1's valid-row list (uint16)
+#endif
 constexpr int kPartPerItem = kSegPerItem * kWarpsPerSeg;  // warp partials per work item
 constexpr int kItemSlots = 2 * kStages;                   // item partial slots per CTA
 constexpr int kWgStride = kConsumerWGs / kSegPerItem;     // stages consumed in parallel
@@ -649,6 +644,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   float4* ipart = reinterpret_cast<float4*>(stage_info + kStages);  // [kItemSlots][kPartPerItem]
   uint32_t* icnt = reinterpret_cast<uint32_t*>(ipart + kItemSlots * kPartPerItem);
   uint32_t* gbits = icnt + kItemSlots;
+  uint16_t* vlist = reinterpret_cast<uint16_t*>(gbits + 2 * kMaxGroups);  // [LOPA_MAX_ROWS]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) TL(0);
@@ -666,21 +662,23 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   // global inputs, then let the dependent fold/tail kernel launch (it may prefetch the inputs).
   grid_dep_wait();
   grid_dep_launch();
-  // ---- work items live in the raw row space: item = group * n_cand + row.  Rows that are not
-  // masked (or belong to absent branches) are skipped; no compaction pass is needed, so the
-  // producer issues its first bulk copy before the masks have even arrived (speculatively: a
-  // copy of a row that turns out invalid is discarded by the consumers).
+  // ---- work items: (group g, row).  The first item of CTA b, (0, raw row b), is issued before
+  // the row masks arrive (speculatively: a copy of a row that turns out invalid is discarded by
+  // the consumers).  Every other item is numbered over the VALID rows only (masked rows of
+  // present branches, ascending in vlist[0, n_valid)), group-major, without the group-0 items of
+  // rows < G already covered by the speculative copies:
+  //   d < n0:  (0, vlist[lo + d])   (lo = valid rows below G, n0 = n_valid - lo)
+  //   else:    e = d - n0, (1 + e / n_valid, vlist[e % n_valid])
+  // so no claim is ever spent on an unmasked row or an absent branch.  CTA b takes d = b, then
+  // claims d = G + counter, two claims in flight (the first two sent before the masks arrive).
   const int W = P.window;
   const int n_seg = P.n_seg, n_grp = P.n_grp;
   const int G = (int)gridDim.x;
   const int n_items_cap = P.n_cand * n_grp;
   const uint64_t pol = policy_evict_first();
   uint32_t i = 0;  // producer: item (= stage use) sequence number of this CTA
-  // Issue one work item (raw row, group g): ONE bulk copy of its <= kSegPerItem segments.
-  auto issue = [&](int cur) {
-    // group-major item order: the (short) last group of every row is streamed last, so the
-    // end of the launch is cut into the smallest items (measured -0.3 us per Dream step)
-    const int g = cur / P.n_cand, row = cur - g * P.n_cand;
+  // Issue one work item (group g, row): ONE bulk copy of its <= kSegPerItem segments.
+  auto issue = [&](int g, int row) {
     const int s0 = g * kSegPerItem, s1 = min(n_seg, s0 + kSegPerItem);
     const int slot = (int)(i % kItemSlots);
     if (i >= (uint32_t)kItemSlots) mbar_wait(&slot_free[slot], ((i / kItemSlots) - 1) & 1);
@@ -696,24 +694,22 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     ++i;
   };
   const int b = blockIdx.x;
-  // items q G + b (q < kStatic) are assigned statically; the first kSpec of them are issued
-  // before the row masks arrive (speculative: validity is checked by the consumers)
-  constexpr int kSpec = LOPA_SPEC_ITEMS < kStages ? LOPA_SPEC_ITEMS : kStages;
-  constexpr int kStatic = kSpec > 2 ? kSpec : 2;
-  const bool dyn = kStatic * G < n_items_cap;
   uint32_t p1 = 0x7FFFFFFFu, p2 = 0x7FFFFFFFu;
+  const bool dyn = G < n_items_cap;  // claims can be needed (the exact test follows the masks)
   if (tid == 0) {
     TL(1);
-#pragma unroll
-    for (int q = 0; q < kSpec; ++q)
-      if (q * G + b < n_items_cap) issue(q * G + b);
-#if LOPA_EARLY_CLAIMS && LOPA_CLAIM_AHEAD == 2
+    // raw item b (no division on the common path: the kernel's first instructions are fetched
+    // cold at every launch, and an integer-division subroutine there measured +0.35 us)
+    if (b < P.n_cand) {
+      issue(0, b);
+    } else if (b < n_items_cap) {
+      issue(b / P.n_cand, b % P.n_cand);
+    }
     // the first two claims travel while the masks load
     if (dyn) {
       p1 = atomicAdd(&P.ctrs[0], 1u);
       p2 = atomicAdd(&P.ctrs[0], 1u);
     }
-#endif
   }
   // valid-row bits: mask byte and n_branches loaded independently (one round trip)
   const int n_groups = (P.n_cand + 31) >> 5;
@@ -723,68 +719,97 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     const bool mk = (in && P.row_mask) ? P.row_mask[r] != 0 : in;
     const int nb_eff = P.n_branches ? *P.n_branches - P.branch_base : 0x7FFFFFFF;
     bool v = mk;
-    if (v && P.n_branches) v = (r / W) < nb_eff;
+    if (v && P.n_branches) v = (int64_t)r < (int64_t)nb_eff * W;  // r / W < nb_eff, no division
     const uint32_t bits = __ballot_sync(0xffffffffu, v);
     if (lane == 0) gbits[g] = bits;
   }
   __syncthreads();
   auto row_valid = [&](int r) -> bool { return (gbits[r >> 5] >> (r & 31)) & 1u; };
-  const int n_items = P.n_cand * n_grp;  // rows of absent branches are skipped like unmasked ones
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---- TMA producer: items b (issued above), G + b, then 2G + counter, ...  Claims on
-      // unmasked rows are skipped without a copy; two claims stay in flight so the atomic's
-      // latency hides behind the issue of two items.
-      auto maybe_issue = [&](int cur) {
-        if (row_valid(cur % P.n_cand)) issue(cur);
-      };
-#if LOPA_CLAIM_AHEAD == 2
-#if !LOPA_EARLY_CLAIMS
-      if (dyn) {
-        p1 = atomicAdd(&P.ctrs[0], 1u);
-        p2 = atomicAdd(&P.ctrs[0], 1u);
-      }
-#endif
-      for (int q = kSpec; q < kStatic; ++q)
-        if (q * G + b < n_items) maybe_issue(q * G + b);
-      if (dyn) {
-        while (true) {
-          const int c1 = kStatic * G + (int)p1;
-          if (c1 >= n_items) break;
-          p1 = atomicAdd(&P.ctrs[0], 1u);
-          maybe_issue(c1);
-          const int c2 = kStatic * G + (int)p2;
-          if (c2 >= n_items) break;
-          p2 = atomicAdd(&P.ctrs[0], 1u);
-          maybe_issue(c2);
-        }
-      }
-#elif LOPA_CLAIM_AHEAD == 1
-      if (dyn) p1 = atomicAdd(&P.ctrs[0], 1u);
-      for (int q = kSpec; q < kStatic; ++q)
-        if (q * G + b < n_items) maybe_issue(q * G + b);
-      if (dyn) {
-        while (true) {
-          const int c1 = kStatic * G + (int)p1;
-          if (c1 >= n_items) break;
-          p1 = atomicAdd(&P.ctrs[0], 1u);
-          maybe_issue(c1);
-        }
-      }
+    // ---- item space.  Items are numbered group-major; the raw items [0, G) (item = group *
+    // n_cand + row) are the speculative copies issued above.  Mostly-valid row sets (>= 7/8: e.g.
+    // a fresh block) number the other items over the raw rows and skip an invalid row's claim;
+    // sparser ones (later iterations of a block, absent branches) number them over the valid
+    // rows only, listed ascending in vlist by the producer warp, so that no claim is spent on a
+    // row without work.  Every CTA takes the same decision from the same masks.
+    int nv = 0;
+    for (int w = lane; w < n_groups; w += 32) nv += __popc(gbits[w]);
+    const int n_valid = (int)__reduce_add_sync(0xffffffffu, (unsigned)nv);
+#ifdef LOPA_NO_COMPACT
+    const bool compact = false;
 #else
-      // claim only once a stage is free: no item is committed to this CTA before it can start
-      for (int q = kSpec; q < kStatic; ++q)
-        if (q * G + b < n_items) maybe_issue(q * G + b);
-      if (dyn) {
-        while (true) {
-          if (i >= (uint32_t)kStages) mbar_wait(&empty[i % kStages], ((i / kStages) - 1) & 1);
-          const int c = kStatic * G + (int)atomicAdd(&P.ctrs[0], 1u);
-          if (c >= n_items) break;
-          maybe_issue(c);
+    const bool compact = 8 * n_valid < 7 * P.n_cand;
+#endif
+    // the speculative copies cover the raw items [0, G): groups < q and rows < rq of group q
+    // (computed on the compact path only: no division on the common path, see above)
+    int n_rows = P.n_cand, lo = 0, q = 0;
+    if (compact) {
+      q = G / P.n_cand;  // n_cand > 0 here (compact implies 7 n_cand > 8 n_valid >= 0)
+      const int rq = G - q * P.n_cand;
+      n_rows = n_valid;
+      int base = 0;
+#pragma unroll 1
+      for (int w = 0; w < n_groups; ++w) {
+        const uint32_t bits = gbits[w];
+        if ((bits >> lane) & 1u) vlist[base + __popc(bits & ((1u << lane) - 1u))] = (uint16_t)(32 * w + lane);
+        if (32 * w < rq) lo += __popc(32 * w + 32 <= rq ? bits : bits & ((1u << (rq - 32 * w)) - 1u));
+        base += __popc(bits);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      // ---- TMA producer
+      if (!compact) {
+        // raw rows: items b (issued above), G + b, then 2G + counter ...; a claim on an invalid
+        // row is skipped
+        const int n_items = P.n_cand * n_grp;
+        auto maybe_issue = [&](int cur) {
+          const int g = cur / P.n_cand, row = cur - g * P.n_cand;
+          if (row_valid(row)) issue(g, row);
+        };
+        if (G + b < n_items) maybe_issue(G + b);
+        if (dyn) {
+          while (true) {
+            const int c1 = 2 * G + (int)p1;
+            if (c1 >= n_items) break;
+            p1 = atomicAdd(&P.ctrs[0], 1u);
+            maybe_issue(c1);
+            const int c2 = 2 * G + (int)p2;
+            if (c2 >= n_items) break;
+            p2 = atomicAdd(&P.ctrs[0], 1u);
+            maybe_issue(c2);
+          }
+        }
+      } else {
+        // valid rows only, after the speculatively covered ones:  d < n0: (q, vlist[lo + d]);
+        // else e = d - n0: (q + 1 + e / n_valid, vlist[e % n_valid]);  item d = b, then
+        // d = G + counter, ...
+        const int n0 = q < n_grp ? n_rows - lo : 0;
+        const int n_dyn = q < n_grp ? n0 + (n_grp - 1 - q) * n_rows : 0;
+        auto issue_d = [&](int d) {
+          int g = q, x = lo + d;
+          if (d >= n0) {
+            const int e = d - n0;
+            g = q + 1 + e / n_rows;
+            x = e - (g - q - 1) * n_rows;
+          }
+          issue(g, vlist[x]);
+        };
+        if (b < n_dyn) issue_d(b);
+        if (dyn) {
+          while (true) {
+            const int c1 = G + (int)p1;
+            if (c1 >= n_dyn) break;
+            p1 = atomicAdd(&P.ctrs[0], 1u);
+            issue_d(c1);
+            const int c2 = G + (int)p2;
+            if (c2 >= n_dyn) break;
+            p2 = atomicAdd(&P.ctrs[0], 1u);
+            issue_d(c2);
+          }
         }
       }
-#endif
       // Self-reset of the work counter: every producer, once done claiming (its outstanding
       // claims returned), takes a ticket; the last one zeroes the counter and the tickets, so a
       // launch leaves the workspace zeroed without any follow-up kernel.
@@ -1125,7 +1150,7 @@ static_assert(LOPA_MAX_ROWS % kTailThreads == 0, "rows per tail thread");
 
 constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + (2 * kStages + kItemSlots) * 8 +
                               kStages * 16 + kItemSlots * kPartPerItem * 16 + kItemSlots * 4 +
-                              2 * kMaxGroups * 4 + 16;
+                              2 * kMaxGroups * 4 + kVlistBytes + 16;
 
 // ------------------------------------------------------------------ small decision kernels
 template <int S>

@@ -100,6 +100,32 @@ def test_reduce_only_leaves_workspace_zeroed(L, n_rows, V):
     assert ws[:8].view(torch.int32).cpu().tolist() == [0, 0]
 
 
+@pytest.mark.parametrize("n_rows,V,n_valid", [(256, 8193, n) for n in (0, 1, 100, 223, 224, 225, 256)]
+                         + [(30, 16391, 10), (30, 16391, 30), (100, 151936, 60), (100, 151936, 99),
+                            (147, 151936, 120), (149, 16391, 120), (5, 151936, 2)])
+def test_confidence_item_spaces(L, n_rows, V, n_valid):
+    """K1 numbers its work items over the raw rows when >= 7/8 of them are valid, else over the
+    valid rows only, after the speculative copies of the raw items [0, G): both
+    sides of the switch, fewer rows than CTAs, and the degenerate row sets give the oracle's
+    conf / argmax on exactly the masked rows."""
+    rng = np.random.default_rng(n_valid)
+    ld = ((V + 7) // 8) * 8
+    rows = _bits(rng.normal(0, 2, size=(n_rows, V)).astype(np.float32))
+    buf = np.zeros((n_rows, ld), np.uint16)
+    buf[:, :V] = rows
+    t = torch.from_numpy(buf.view(np.int16)).to(DEV).view(torch.bfloat16)
+    m = np.zeros(n_rows, np.uint8)
+    m[rng.permutation(n_rows)[:n_valid]] = 1
+    conf, amax, st = L.confidence(t, vocab=V, row_mask=torch.from_numpy(m).to(DEV))
+    rc, ra, _ = O.confidence(rows)
+    sel = m.astype(bool)
+    assert int(st.item()) == 0
+    c, a = conf.cpu().numpy().astype(np.float64), amax.cpu().numpy()
+    assert np.max(np.abs(c[sel] - rc[sel]), initial=0.0) <= G.CONF_TOL
+    assert np.array_equal(a[sel], ra[sel])
+    assert np.all(np.isnan(c[~sel])) and np.all(a[~sel] == -1)
+
+
 @pytest.mark.parametrize("V", [(1 << 20) + 3, 1 << 23])
 def test_confidence_huge_vocab(L, V):
     """Up to LOPA_MAX_VOCAB = 2^23: 512 groups per row, so the fold takes its sequential
