@@ -84,6 +84,12 @@ typedef enum {
 
 int lopa_version(void);
 const char* lopa_status_string(int status);
+/* The CUDA runtime's message for the last call of this thread that returned LOPA_ERR_CUDA
+ * ("" if none).  The string is owned by the library and valid until the next such call. */
+const char* lopa_last_cuda_error(void);
+/* Debug: {registers/thread, max threads/block, static shared bytes, local bytes/thread, block
+ * size launched} of the vocabulary-reduction kernel K1 this build uses. */
+int lopa_debug_k1_attrs(int32_t* out5);
 
 /* Bytes of device workspace needed for up to max_rows rows of `vocab` logits. */
 size_t lopa_workspace_bytes(int32_t max_rows, int32_t vocab);
@@ -260,6 +266,13 @@ int lopa_debug_reduce_only(const void* logits_bf16, int64_t ld, int32_t n_rows, 
  * Slots: 0 CTA start, 1 producer start, 2 first stage consumed, 3 last unit consumed,
  * 4 tail start, 5 tail end. */
 int lopa_debug_timeline(unsigned long long* out, int n_ctas);
+/* Debug: per-warp timeline of the warp-staged K1's last launch (experiment builds with
+ * -DLOPA_LDG_TL only).  Returns the words written, minus the words needed if n_words is too
+ * small, 0 if the build has no timeline. */
+int lopa_debug_ldg_timeline(unsigned long long* out, int n_words);
+/* Debug: per-item timeline of the TMA-form K1's last launch (-DLOPA_K1_TL builds only); same
+ * return convention. */
+int lopa_debug_k1_timeline(unsigned long long* out, int n_words);
 
 /* ---------------------------------------------------------------- harness (not the method)
  * SYN-D2F synthetic logits for a batch of branch states (the stand-in for the dLLM forward;

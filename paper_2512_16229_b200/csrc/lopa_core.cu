@@ -634,6 +634,33 @@ __device__ void cta_tail_bp_local(const Params& P, TailSmem& T, int tid, int nb)
 }
 
 // ------------------------------------------------------------------ the fused kernel
+#ifdef LOPA_K1_TL
+// experiment: per-item %globaltimer stamps of K1's TMA form (lopa_debug_k1_timeline):
+// [cta][0..95]: producer (wait begin, issue) per item < 48; [cta][96 + 48 wg + 3 n + x]:
+// consumer warpgroup wg, its n-th stage (full-wait return, release, partial done)
+constexpr int kK1TlWords = 96 + 6 * 48;
+__device__ unsigned long long g_k1tl[160][kK1TlWords];
+__device__ __forceinline__ unsigned long long k1_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define K1TL(idx) (g_k1tl[blockIdx.x][(idx)] = k1_gtime())
+#else
+#define K1TL(idx) ((void)0)
+#endif
+// A work claim.  LOPA_TMA_ASM_ATOM: one atom instruction whose value is waited for where it is
+// used (atomicAdd is warp-aggregated by the compiler: vote + shuffle of the returned value,
+// which waits for the round trip at the call).
+#ifndef LOPA_STATIC_PCT
+#define LOPA_STATIC_PCT 0
+#endif
+constexpr int kStaticPct = LOPA_STATIC_PCT;  // % of K1's items assigned statically
+#ifdef LOPA_TMA_ASM_ATOM
+#define K1_CLAIM(p) atom_add_u32((p), 1u)
+#else
+#define K1_CLAIM(p) atomicAdd((p), 1u)
+#endif
 __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel(const Params P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* stages = smem;
@@ -681,9 +708,11 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   auto issue = [&](int g, int row) {
     const int s0 = g * kSegPerItem, s1 = min(n_seg, s0 + kSegPerItem);
     const int slot = (int)(i % kItemSlots);
+    if (i < 48) K1TL(2 * i);
     if (i >= (uint32_t)kItemSlots) mbar_wait(&slot_free[slot], ((i / kItemSlots) - 1) & 1);
     const int s = (int)(i % kStages);
     if (i >= (uint32_t)kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+    if (i < 48) K1TL(2 * i + 1);
     stage_info[s] = make_int4(row, g, slot, s1 - s0);
     const int e0 = s0 * P.seg_len;
     const int e1 = min(P.vocab, s1 * P.seg_len);
@@ -707,8 +736,8 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     }
     // the first two claims travel while the masks load
     if (dyn) {
-      p1 = atomicAdd(&P.ctrs[0], 1u);
-      p2 = atomicAdd(&P.ctrs[0], 1u);
+      p1 = K1_CLAIM(&P.ctrs[0]);
+      p2 = K1_CLAIM(&P.ctrs[0]);
     }
   }
   // valid-row bits: mask byte and n_branches loaded independently (one round trip)
@@ -716,10 +745,11 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   for (int g = warp; g < n_groups; g += kWarps) {
     const int r = g * 32 + lane;
     const bool in = r < P.n_cand;
-    const bool mk = (in && P.row_mask) ? P.row_mask[r] != 0 : in;
     const int nb_eff = P.n_branches ? *P.n_branches - P.branch_base : 0x7FFFFFFF;
-    bool v = mk;
-    if (v && P.n_branches) v = (int64_t)r < (int64_t)nb_eff * W;  // r / W < nb_eff, no division
+    // r / W < nb_eff (no division); the mask byte is read only for rows of present branches,
+    // so a rank whose shard runs past the table's last branch never reads beyond it
+    bool v = in && (!P.n_branches || (int64_t)r < (int64_t)nb_eff * W);
+    if (v && P.row_mask) v = P.row_mask[r] != 0;
     const uint32_t bits = __ballot_sync(0xffffffffu, v);
     if (lane == 0) gbits[g] = bits;
   }
@@ -760,33 +790,39 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     }
     if (lane == 0) {
       // ---- TMA producer
+      // The first rounds of items are assigned statically (CTA b takes item j G + b of round j:
+      // no claim round trip on the producer's path while HBM is saturated); the last
+      // ~(100 - LOPA_STATIC_PCT)% are claimed dynamically, two claims in flight, to balance the
+      // end of the launch.  The round count depends only on the item count (the same in every CTA).
       if (!compact) {
-        // raw rows: items b (issued above), G + b, then 2G + counter ...; a claim on an invalid
-        // row is skipped
+        // raw rows: items b (issued above), G + b, ..., (S - 1) G + b, then S G + counter ...; an
+        // invalid row's item is skipped
         const int n_items = P.n_cand * n_grp;
+        const int S = max(2, (int)((int64_t)n_items * kStaticPct / 100) / G);
         auto maybe_issue = [&](int cur) {
           const int g = cur / P.n_cand, row = cur - g * P.n_cand;
           if (row_valid(row)) issue(g, row);
         };
-        if (G + b < n_items) maybe_issue(G + b);
+        for (int jr = 1; jr < S && jr * G + b < n_items; ++jr) maybe_issue(jr * G + b);
         if (dyn) {
           while (true) {
-            const int c1 = 2 * G + (int)p1;
+            const int c1 = S * G + (int)p1;
             if (c1 >= n_items) break;
-            p1 = atomicAdd(&P.ctrs[0], 1u);
+            p1 = K1_CLAIM(&P.ctrs[0]);
             maybe_issue(c1);
-            const int c2 = 2 * G + (int)p2;
+            const int c2 = S * G + (int)p2;
             if (c2 >= n_items) break;
-            p2 = atomicAdd(&P.ctrs[0], 1u);
+            p2 = K1_CLAIM(&P.ctrs[0]);
             maybe_issue(c2);
           }
         }
       } else {
         // valid rows only, after the speculatively covered ones:  d < n0: (q, vlist[lo + d]);
-        // else e = d - n0: (q + 1 + e / n_valid, vlist[e % n_valid]);  item d = b, then
-        // d = G + counter, ...
+        // else e = d - n0: (q + 1 + e / n_valid, vlist[e % n_valid]);  items d = b, G + b, ...,
+        // (S - 1) G + b, then d = S G + counter, ...
         const int n0 = q < n_grp ? n_rows - lo : 0;
         const int n_dyn = q < n_grp ? n0 + (n_grp - 1 - q) * n_rows : 0;
+        const int S = max(1, (int)((int64_t)n_dyn * kStaticPct / 100) / G);
         auto issue_d = [&](int d) {
           int g = q, x = lo + d;
           if (d >= n0) {
@@ -796,16 +832,16 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
           }
           issue(g, vlist[x]);
         };
-        if (b < n_dyn) issue_d(b);
+        for (int jr = 0; jr < S && jr * G + b < n_dyn; ++jr) issue_d(jr * G + b);
         if (dyn) {
           while (true) {
-            const int c1 = G + (int)p1;
+            const int c1 = S * G + (int)p1;
             if (c1 >= n_dyn) break;
-            p1 = atomicAdd(&P.ctrs[0], 1u);
+            p1 = K1_CLAIM(&P.ctrs[0]);
             issue_d(c1);
-            const int c2 = G + (int)p2;
+            const int c2 = S * G + (int)p2;
             if (c2 >= n_dyn) break;
-            p2 = atomicAdd(&P.ctrs[0], 1u);
+            p2 = K1_CLAIM(&P.ctrs[0]);
             issue_d(c2);
           }
         }
@@ -836,9 +872,15 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     const int wq = (warp - 1) & 3;
     const int jseg = wg % kSegPerItem;
     bool first = true;
+#ifdef LOPA_K1_TL
+    int tln = 0;
+#endif
     for (uint32_t i = wg / kSegPerItem;; i += kWgStride) {
       const int s = (int)(i % kStages);
       mbar_wait(&full[s], (i / kStages) & 1);
+#ifdef LOPA_K1_TL
+      if (wq == 0 && lane == 0 && tln < 16) K1TL(96 + 48 * wg + 3 * tln);
+#endif
       if (first && warp == 1 && lane == 0) TL(2);
       first = false;
       const int4 info = stage_info[s];
@@ -856,6 +898,9 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
       const int nchunks = (e1 - e0 + 7) >> 3;
       const Partial pr = reduce_slice(stages + (size_t)s * kStageBytes + (size_t)jseg * P.seg_len * 2,
                                       nchunks, e0, P.vocab, wq, lane, &empty[s]);
+#ifdef LOPA_K1_TL
+      if (wq == 0 && lane == 0 && tln < 16) { K1TL(96 + 48 * wg + 3 * tln + 2); ++tln; }
+#endif
       uint32_t done = 0;
       if (lane == 0) {
         ipart[slot * kPartPerItem + jseg * kWarpsPerSeg + wq] =
@@ -878,6 +923,405 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
 
   if (tid == 0) TL(4);
 }
+
+// ------------------------------------------------------------------ K1, warp-staged form
+// EXPERIMENT (built only with -DLOPA_K1_LDG; not in the product library).  Bit-identical to the
+// TMA form and parity-green on the B200, but 1.9x slower on the Dream step (DESIGN.md §5,
+// profiles/r02_k1_ab.md): the per-warp cp.async streams reach ~25 GB/s per SM where the TMA
+// ring reaches ~45.
+#ifdef LOPA_K1_LDG
+// The same work items, canonical slices and folds as lopa_reduce_kernel (so the group partials
+// are bit-identical), but with no shared TMA stage: every consumer warp streams its own slice
+// of an item through a private ring of shared-memory buffers with 16-byte cp.async copies, and
+// waits for them with cp.async.wait_group (per-thread commit groups complete in order, so a
+// warp keeps kLDepth slices in flight while it reduces the oldest one):
+//   * kTeams teams of 8 warps and no producer warp.  Warp (jseg, wq) of a team reduces chunks
+//     c = 128 i + 32 wq + lane (i < 8) of segment jseg of each of the team's items -- exactly
+//     reduce_slice's quarter; each lane copies and later reads only its own chunks.
+//   * Lane 0 of the team's first warp (the team leader) publishes the team's item descriptors
+//     into the team's ring of kLSlots slots (mbarrier `ready` per slot; a slot is reused once its
+//     item is folded, mbarrier `sfree`), kLDepth + 1 items ahead of its own reduction.  It keeps
+//     two claims on the global work counter in flight: a claim's value is consumed one publish
+//     after it is issued, so the atomic's round trip hides behind the team's work.
+//   * The first item of the first kLSpec teams of CTA b is the raw item t G + b, published and
+//     copied before the row masks arrive (a copy of a row that turns out invalid is discarded).
+//     Further items follow K1's numbering: raw items n_spec + claim over mostly-valid row sets
+//     (a claim on an invalid row is skipped), otherwise items numbered over the valid rows only
+//     (vlist), group-major.
+//   * All 8 warps of an item count into icnt; the last one folds the item's warp partials
+//     (fold_seq, fixed order) into the group partial, as K1's TMA form does.
+// (A first form that loaded the slices straight into two register buffers per warp lost all
+// overlap: ptxas gives every LDG the same scoreboard, so reducing one buffer waited for the
+// other buffer's loads too.  Commit groups make the wait explicit.)
+#ifndef LOPA_LDG_TEAMS
+#define LOPA_LDG_TEAMS 2
+#endif
+#ifndef LOPA_LDG_DEPTH
+#define LOPA_LDG_DEPTH 2
+#endif
+#ifndef LOPA_LDG_SLOTS
+#define LOPA_LDG_SLOTS (LOPA_LDG_DEPTH + 2)
+#endif
+#ifndef LOPA_LDG_SPEC
+#define LOPA_LDG_SPEC 1
+#endif
+constexpr int kTeams = LOPA_LDG_TEAMS;
+constexpr int kTeamWarps = kSegPerItem * kWarpsPerSeg;  // one warp per (segment, quarter)
+constexpr int kLThreads = 32 * kTeamWarps * kTeams;
+constexpr int kLDepth = LOPA_LDG_DEPTH;  // slices in flight per warp beyond the one reduced
+constexpr int kLBufs = kLDepth + 1;
+constexpr int kLSlots = LOPA_LDG_SLOTS;  // item slots per team
+constexpr int kLSpec = LOPA_LDG_SPEC;    // teams whose first item is speculative
+constexpr int kSliceChunks = kChunksPerLane * 32;  // 16-byte chunks of one warp slice (4 KB)
+constexpr size_t kLSmemBytes = (size_t)kTeams * kTeamWarps * kLBufs * kSliceChunks * 16;
+// The leader publishes item k + kLDepth + 1 before reducing item k: that item's slot must have
+// been freed by item k - 1, which every warp of the team has reduced before reaching item k.
+static_assert(kLSlots >= kLDepth + 2, "item ring too short for the staging depth");
+static_assert(kLSpec >= 0 && kLSpec <= kTeams, "speculative teams");
+static_assert(kLDepth >= 1, "at least one slice in flight");
+static_assert(kTeamWarps * 32 == 256, "team = 8 warps");
+
+// reduce_slice's arithmetic on a slice already in registers (identical operations and order,
+// so identical bits); the first-argmax chunk is selected from the registers.
+__device__ __forceinline__ Partial reduce_regs(uint4 (&v)[kChunksPerLane], int nchunks, int e0,
+                                               int vocab, int wq, int lane) {
+  const bool ragged = (vocab & 7) != 0;
+  if (ragged) {
+#pragma unroll
+    for (int t = 0; t < kChunksPerLane; ++t) {
+      const int c = 128 * t + 32 * wq + lane;
+      const int nvalid = vocab - (e0 + 8 * c);
+      if (c < nchunks && nvalid < 8) mask_tail(v[t], nvalid);
+    }
+  }
+  uint32_t cm[kChunksPerLane];
+#pragma unroll
+  for (int t = 0; t < kChunksPerLane; ++t) cm[t] = bmax2(bmax2(v[t].x, v[t].y), bmax2(v[t].z, v[t].w));
+  uint32_t mm = cm[0];
+#pragma unroll
+  for (int t = 1; t < kChunksPerLane; ++t) mm = bmax2(mm, cm[t]);
+  const float ml = fmax_nan(bf16lo(mm), bf16hi(mm));
+  const float m = unordered(__reduce_max_sync(0xffffffffu, ordered_bits(ml)));
+  Partial p;
+  p.m = m;
+  if (m == -INFINITY) {  // warp-uniform: every element is -inf (or NaN)
+    bool bad = false;
+#pragma unroll
+    for (int t = 0; t < kChunksPerLane; ++t) bad |= chunk_has_nan(v[t]);
+    p.s = __any_sync(0xffffffffu, bad) ? __int_as_float(0x7FC00000) : 0.f;
+    p.a = 0xFFFFFFFFu;
+    return p;
+  }
+  uint32_t cand = 0xFFFFFFFFu;
+  if (ml == m) {
+    const __nv_bfloat162 m2 = __floats2bfloat162_rn(m, m);
+    int tf = kChunksPerLane - 1;
+#pragma unroll
+    for (int t = kChunksPerLane - 1; t >= 0; --t)
+      if (!__hbne2(*reinterpret_cast<const __nv_bfloat162*>(&cm[t]), m2)) tf = t;
+    uint4 w = v[0];
+#pragma unroll
+    for (int t = 1; t < kChunksPerLane; ++t)
+      if (tf == t) w = v[t];
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    int ef = 7;
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+      const unsigned eq = __heq2_mask(*reinterpret_cast<const __nv_bfloat162*>(&ws[j]), m2);
+      if (eq) ef = 2 * j + ((eq & 0xFFFFu) ? 0 : 1);
+    }
+    cand = (uint32_t)(e0 + 8 * (128 * tf + 32 * wq + lane) + ef);
+  }
+  const float negm = -m;
+  float2 acc = chunk_exp_sum2(v[0], negm);
+#pragma unroll
+  for (int t = 1; t < kChunksPerLane; ++t) acc = __fadd2_rn(acc, chunk_exp_sum2(v[t], negm));
+  float ls = acc.x + acc.y;
+  p.a = __reduce_min_sync(0xffffffffu, cand);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
+  p.s = ls;
+  return p;
+}
+
+#ifdef LOPA_LDG_TL
+// experiment: per-warp %globaltimer stamps of the warp-staged K1 (lopa_debug_ldg_timeline)
+constexpr int kLtlItems = 40;
+__device__ unsigned long long g_ldg_tl[160][kLThreads / 32][2 + 3 * kLtlItems];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+__global__ void __launch_bounds__(kLThreads, 1) lopa_reduce_ldg_kernel(const Params P) {
+  extern __shared__ __align__(128) uint8_t lsm[];  // [warp][kLBufs][kSliceChunks] 16-byte chunks
+  // per team: slot ring of item descriptors (row, group, segments in the item, -); row -1 = end
+  // of the team's work, -2 = no item
+  __shared__ int4 sinfo[kTeams][kLSlots];
+  __shared__ __align__(8) uint64_t ready[kTeams][kLSlots];
+  __shared__ __align__(8) uint64_t sfree[kTeams][kLSlots];
+  __shared__ float4 ipart[kTeams][kLSlots][kTeamWarps];
+  __shared__ uint32_t icnt[kTeams][kLSlots];
+  __shared__ uint32_t gbits[2 * kMaxGroups];
+  __shared__ uint16_t vlist[kTeams][LOPA_MAX_ROWS];  // a team leader's valid-row list
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int team = warp / kTeamWarps, j = warp % kTeamWarps;
+  const int jseg = j / kWarpsPerSeg, wq = j % kWarpsPerSeg;
+  const bool leader = j == 0 && lane == 0;
+  const int W = P.window;
+  const int n_seg = P.n_seg, n_grp = P.n_grp;
+  const int G = (int)gridDim.x;
+  const int b = blockIdx.x;
+  const int n_items_cap = P.n_cand * n_grp;
+  const int n_spec = kLSpec * G;  // raw items [0, n_spec) are speculative first items
+  const bool dyn = n_spec < n_items_cap;
+  const uint64_t pol = policy_evict_first();
+  uint4* bufs = reinterpret_cast<uint4*>(lsm) + (size_t)warp * kLBufs * kSliceChunks + lane;
+#ifdef LOPA_LDG_TL
+  unsigned long long* tl = g_ldg_tl[blockIdx.x][warp];
+  if (lane == 0) tl[0] = gtime();
+#endif
+  if (tid < kTeams * kLSlots) {
+    mbar_init(&ready[0][0] + tid, 1);
+    mbar_init(&sfree[0][0] + tid, 1);
+    (&icnt[0][0])[tid] = 0;
+  }
+  fence_mbar_init();
+  grid_dep_wait();
+  grid_dep_launch();
+  __syncthreads();  // mbarrier inits
+
+  uint32_t u = 0;  // leader: items published so far by its team
+  auto publish = [&](int row, int g) {
+    const int slot = (int)(u % kLSlots);
+    if (u >= (uint32_t)kLSlots) mbar_wait(&sfree[team][slot], ((u / kLSlots) - 1) & 1);
+    const int s0 = g * kSegPerItem;
+    sinfo[team][slot] = make_int4(row, g, row >= 0 ? min(n_seg, s0 + kSegPerItem) - s0 : 0, 0);
+    mbar_arrive(&ready[team][slot]);
+    ++u;
+  };
+  uint32_t p1 = 0x7FFFFFFFu, p2 = 0x7FFFFFFFu;
+  if (leader) {
+    if (team < kLSpec) {
+      const int r = team * G + b;  // no division for the common first item
+      if (r < P.n_cand) publish(r, 0);
+      else if (r < n_items_cap) publish(r % P.n_cand, r / P.n_cand);
+      else publish(-2, 0);
+    }
+    if (dyn) {  // the first two claims travel while the masks load
+      p1 = atom_add_u32(&P.ctrs[0], 1u);
+      p2 = atom_add_u32(&P.ctrs[0], 1u);
+    }
+  }
+  struct Task {
+    int row, g, slot, nsi;
+  };
+  auto fetch = [&](uint32_t k) -> Task {
+    const int slot = (int)(k % kLSlots);
+    mbar_wait(&ready[team][slot], (k / kLSlots) & 1);
+    const int4 in = sinfo[team][slot];
+    return Task{in.x, in.y, slot, in.z};
+  };
+  auto seg_geom = [&](const Task& t, int* e0, int* nch) {
+    const int seg = t.g * kSegPerItem + jseg;
+    *e0 = seg * P.seg_len;
+    const int e1 = min(P.vocab, *e0 + P.seg_len);
+    *nch = (e1 - *e0 + 7) >> 3;
+  };
+  // copy this warp's slice of item t into buffer `buf` (this lane's chunks only)
+  auto stage = [&](const Task& t, int buf) {
+    int e0, nch;
+    seg_geom(t, &e0, &nch);
+    const uint4* src = reinterpret_cast<const uint4*>(P.logits + (size_t)t.row * P.ld + e0);
+    uint4* dst = bufs + buf * kSliceChunks;
+#pragma unroll
+    for (int i = 0; i < kChunksPerLane; ++i) {
+      const int c = 128 * i + 32 * wq + lane;
+      if (c < nch) cp_async16(dst + 32 * i, src + c, pol);
+    }
+  };
+  if (team < kLSpec) {
+    // the speculative first item: its copies leave before the masks arrive
+    const Task t = fetch(0);
+    if (t.row >= 0 && jseg < t.nsi) stage(t, 0);
+    cp_async_commit();
+  }
+  // valid-row bits: mask byte and n_branches loaded independently (one round trip)
+  const int n_groups = (P.n_cand + 31) >> 5;
+  for (int gq = warp; gq < n_groups; gq += kLThreads / 32) {
+    const int r = gq * 32 + lane;
+    const bool in = r < P.n_cand;
+    const int nb_eff = P.n_branches ? *P.n_branches - P.branch_base : 0x7FFFFFFF;
+    // the mask byte is read only for rows of present branches (r / W < nb_eff)
+    bool v = in && (!P.n_branches || (int64_t)r < (int64_t)nb_eff * W);
+    if (v && P.row_mask) v = P.row_mask[r] != 0;
+    const uint32_t bits = __ballot_sync(0xffffffffu, v);
+    if (lane == 0) gbits[gq] = bits;
+  }
+  __syncthreads();
+  auto row_valid = [&](int r) -> bool { return (gbits[r >> 5] >> (r & 31)) & 1u; };
+
+  // ---- the leader warp's item space (the same decision in every team of every CTA)
+  bool compact = false;
+  int n_rows = P.n_cand, lo = 0, q = 0, n0 = 0, n_dyn = 0;
+  if (j == 0) {
+    int nv = 0;
+    for (int w = lane; w < n_groups; w += 32) nv += __popc(gbits[w]);
+    const int n_valid = (int)__reduce_add_sync(0xffffffffu, (unsigned)nv);
+#ifndef LOPA_NO_COMPACT
+    compact = 8 * n_valid < 7 * P.n_cand;
+#endif
+    if (compact) {
+      q = n_spec / P.n_cand;  // n_cand > 0 here
+      const int rq = n_spec - q * P.n_cand;
+      n_rows = n_valid;
+      int base = 0;
+#pragma unroll 1
+      for (int w = 0; w < n_groups; ++w) {
+        const uint32_t bits = gbits[w];
+        if ((bits >> lane) & 1u) vlist[team][base + __popc(bits & ((1u << lane) - 1u))] = (uint16_t)(32 * w + lane);
+        if (32 * w < rq) lo += __popc(32 * w + 32 <= rq ? bits : bits & ((1u << (rq - 32 * w)) - 1u));
+        base += __popc(bits);
+      }
+      __syncwarp();
+      n0 = q < n_grp ? n_rows - lo : 0;
+      n_dyn = q < n_grp ? n0 + (n_grp - 1 - q) * n_rows : 0;
+    } else {
+      n_dyn = dyn ? n_items_cap - n_spec : 0;
+    }
+  }
+  // Leader: publish the team's next item from the oldest claim (the end sentinel once the claims
+  // run out), and keep two claims in flight.  Returns false once the sentinel is published.
+  bool claiming = dyn;
+  auto publish_next = [&]() -> bool {
+    while (claiming) {
+      const int d = (int)p1;
+      if (d >= n_dyn) {
+        claiming = false;
+        break;
+      }
+      p1 = p2;
+      p2 = atom_add_u32(&P.ctrs[0], 1u);
+      if (compact) {
+        int g = q, x = lo + d;
+        if (d >= n0) {
+          const int e = d - n0;
+          g = q + 1 + e / n_rows;
+          x = e - (g - q - 1) * n_rows;
+        }
+        publish(vlist[team][x], g);
+        return true;
+      }
+      const int c = n_spec + d;
+      const int g = c / P.n_cand, row = c - g * P.n_cand;
+      if (row_valid(row)) {
+        publish(row, g);
+        return true;
+      }
+    }
+    // done claiming: every outstanding claim has returned (p1, p2 consumed); the last of all
+    // the leaders to get here zeroes the counter (K1 leaves the workspace zeroed)
+    asm volatile("" ::"r"(p1), "r"(p2));
+    if (dyn) {
+      __threadfence();
+      if (atomicAdd(&P.ctrs[1], 1u) == (uint32_t)(G * kTeams) - 1) {
+        __threadfence();
+        P.ctrs[0] = 0;
+        P.ctrs[1] = 0;
+      }
+    }
+    publish(-1, 0);
+    return false;
+  };
+  bool more = true;  // leader: items remain to be published
+  auto ensure_published = [&](uint32_t last) {  // items 0 .. last (or up to the sentinel)
+    while (more && u <= last) more = publish_next();
+  };
+
+  // ---- reduce item t from buffer `buf`; the last of the 8 warps folds the item
+  auto consume = [&](const Task& t, int buf) {
+    const bool valid = t.row >= 0 && row_valid(t.row);
+    if (valid && jseg < t.nsi) {
+      int e0, nch;
+      seg_geom(t, &e0, &nch);
+      const uint4* src = bufs + buf * kSliceChunks;
+      uint4 v[kChunksPerLane];
+#pragma unroll
+      for (int i = 0; i < kChunksPerLane; ++i) {
+        const int c = 128 * i + 32 * wq + lane;
+        v[i] = (c < nch) ? lds128(src + 32 * i)
+                         : make_uint4(kNegInfBf16x2, kNegInfBf16x2, kNegInfBf16x2, kNegInfBf16x2);
+      }
+#ifdef LOPA_LDG_NOCOMPUTE
+      // streaming experiment: consume the slice and return a dummy partial
+      uint32_t acc = 0;
+#pragma unroll
+      for (int i = 0; i < kChunksPerLane; ++i) acc ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
+      Partial pr;
+      pr.m = 0.f;
+      pr.s = 1.0f + (acc == 0x12345678u ? 1.f : 0.f);
+      pr.a = 0;
+      (void)e0;
+#else
+      const Partial pr = reduce_regs(v, nch, e0, P.vocab, wq, lane);
+#endif
+      if (lane == 0) ipart[team][t.slot][jseg * kWarpsPerSeg + wq] = make_float4(pr.m, pr.s, __uint_as_float(pr.a), 0.f);
+    }
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd_block(&icnt[team][t.slot], 1u) + 1u == (uint32_t)kTeamWarps) {
+        __threadfence_block();
+        if (valid) {
+          const float4* qp = ipart[team][t.slot];
+          const FoldAcc f = fold_seq(kWarpsPerSeg * t.nsi, [&](int p) { return qp[p]; });
+          P.gpart[(size_t)t.g * P.n_cand + t.row] = make_float4(f.M, f.S, __uint_as_float(f.a), 0.f);
+        }
+        icnt[team][t.slot] = 0;
+        mbar_arrive(&sfree[team][t.slot]);
+      }
+    }
+    __syncwarp();
+  };
+
+  // ---- stage kLDepth items ahead; one commit group per item (empty once the end is staged)
+  uint32_t k_staged = team < kLSpec ? 1u : 0u;  // next item to stage
+  uint32_t k_end = 0xFFFFFFFFu;                 // the item holding the end sentinel
+  auto stage_next = [&]() {
+    if (k_end == 0xFFFFFFFFu) {
+      const Task t = fetch(k_staged);
+      if (t.row == -1) k_end = k_staged;
+      else if (t.row >= 0 && jseg < t.nsi && row_valid(t.row)) stage(t, (int)(k_staged % kLBufs));
+      ++k_staged;
+    }
+    cp_async_commit();
+  };
+  if (leader) ensure_published(kLDepth);
+  for (uint32_t c = k_staged; c < (uint32_t)kLDepth; ++c) stage_next();
+#ifdef LOPA_LDG_TL
+  if (lane == 0) tl[1] = gtime();
+#endif
+  for (uint32_t k = 0;; ++k) {
+#ifdef LOPA_LDG_TL
+    if (lane == 0 && k < kLtlItems) tl[2 + 3 * k] = gtime();
+#endif
+    if (leader) ensure_published(k + kLDepth + 1);
+    stage_next();               // item k + kLDepth
+    cp_async_wait<kLDepth>();   // item k has landed
+#ifdef LOPA_LDG_TL
+    if (lane == 0 && k < kLtlItems) tl[3 + 3 * k] = gtime();
+#endif
+    if (k == k_end) break;
+    const int slot = (int)(k % kLSlots);
+    const int4 in = sinfo[team][slot];
+    consume(Task{in.x, in.y, slot, in.z}, (int)(k % kLBufs));
+#ifdef LOPA_LDG_TL
+    if (lane == 0 && k < kLtlItems) tl[4 + 3 * k] = gtime();
+#endif
+  }
+}
+#endif  // LOPA_K1_LDG
 
 // ------------------------------------------------------------------ K2: fold + decisions
 // One CTA, launched programmatically dependent on K1: its launch and prologue overlap K1, and
@@ -1332,16 +1776,22 @@ static int ensure_kernel_attrs(int device) {
       cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device) != cudaSuccess)
     return LOPA_ERR_CUDA;
   if (major != 10 || minor != 0) return LOPA_ERR_UNSUPPORTED;
-  if (cudaFuncSetAttribute(lopa_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kSmemBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(lopa_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kFoldSmemBytes) != cudaSuccess)
-    return LOPA_ERR_CUDA;
+  cudaError_t e = cudaFuncSetAttribute(lopa_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(lopa_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kFoldSmemBytes);
+#ifdef LOPA_K1_LDG
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(lopa_reduce_ldg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kLSmemBytes);
+#endif
   for (int mode : {(int)MODE_STEP, (int)MODE_BP_LOCAL, (int)MODE_DECIDE})
     for (int w : {32, 64, 256})
-      if (cudaFuncSetAttribute(tail_kernel_for(mode, w), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kTailSmemBytes) != cudaSuccess)
-        return LOPA_ERR_CUDA;
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tail_kernel_for(mode, w), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kTailSmemBytes);
+  if (e != cudaSuccess) return cuda_status(e);
   std::lock_guard<std::mutex> lk(g_mu);
   if (device >= 0 && device < 64) g_attr[device] = true;
   return LOPA_OK;
@@ -1432,21 +1882,34 @@ static void prof_record(int which, cudaStream_t s, int* slot) {
 
 // K1 (streaming reduction) then K2 (fold + decisions, or the fold only for MODE_CONF), both
 // with programmatic dependent launch so launch latency overlaps the previous kernel.
+// K1's form: register-fed (lopa_reduce_ldg_kernel) or TMA-ring (lopa_reduce_kernel).
+#ifdef LOPA_K1_LDG
+#define LOPA_K1_KERNEL lopa_reduce_ldg_kernel
+constexpr int kK1Threads = kLThreads;
+constexpr size_t kK1Smem = kLSmemBytes;
+constexpr int kK1CtasPerSm = 1;
+#else
+#define LOPA_K1_KERNEL lopa_reduce_kernel
+constexpr int kK1Threads = kThreads;
+constexpr size_t kK1Smem = kSmemBytes;
+constexpr int kK1CtasPerSm = LOPA_CTAS_PER_SM;
+#endif
+
 static int launch_reduce(const Params& P, int device, cudaStream_t s, bool k1_only = false) {
   int st = ensure_kernel_attrs(device);
   if (st != LOPA_OK) return st;
   if (k1_only) {  // measurement: K1 alone, in the step's launch configuration
-    const int g = LOPA_CTAS_PER_SM * (num_sms(device) - 1);
-    return cuda_status(launch_pdl(lopa_reduce_kernel, dim3(g), dim3(kThreads), kSmemBytes, s, P));
+    const int g = kK1CtasPerSm * (num_sms(device) - 1);
+    return cuda_status(launch_pdl(LOPA_K1_KERNEL, dim3(g), dim3(kK1Threads), kK1Smem, s, P));
   }
   // One SM is left to the fold/tail kernel: it becomes resident there while K1 streams (PDL)
   // and, landing on the same SM step after step, runs with a warm instruction cache.
-  const int grid = LOPA_CTAS_PER_SM * (num_sms(device) - (P.mode == MODE_CONF ? 0 : 1));
+  const int grid = kK1CtasPerSm * (num_sms(device) - (P.mode == MODE_CONF ? 0 : 1));
   if (grid <= 0) return LOPA_ERR_CUDA;
   int pslot = -1;
   prof_record(0, s, &pslot);
-  cudaError_t e = launch_pdl(lopa_reduce_kernel, dim3(grid), dim3(kThreads), kSmemBytes, s, P);
-  if (e != cudaSuccess) return LOPA_ERR_CUDA;
+  cudaError_t e = launch_pdl(LOPA_K1_KERNEL, dim3(grid), dim3(kK1Threads), kK1Smem, s, P);
+  if (e != cudaSuccess) return cuda_status(e);
   prof_record(1, s, &pslot);
   if (P.mode == MODE_CONF) {
     const int nb = (P.n_cand + 255) / 256;
@@ -1608,6 +2071,13 @@ using namespace lopa;
 
 extern "C" int lopa_version(void) { return LOPA_VERSION; }
 
+static thread_local char g_last_cuda_error[256];
+void lopa::note_cuda_error(cudaError_t e) {
+  snprintf(g_last_cuda_error, sizeof(g_last_cuda_error), "%s: %s", cudaGetErrorName(e),
+           cudaGetErrorString(e));
+}
+extern "C" const char* lopa_last_cuda_error(void) { return g_last_cuda_error; }
+
 extern "C" int lopa_profile_enable(int32_t max_records) {
   if (max_records < 1) return LOPA_ERR_INVALID_ARG;
   std::lock_guard<std::mutex> lk(lopa::g_prof.mu);
@@ -1659,6 +2129,49 @@ extern "C" int lopa_debug_timeline(unsigned long long* out, int n_ctas) {
   (void)out; (void)n_ctas;
   return 0;
 #endif
+}
+
+// Debug (LOPA_K1_TL builds): per-item timeline of K1's TMA form, last launch.
+extern "C" int lopa_debug_k1_timeline(unsigned long long* out, int n_words) {
+#ifdef LOPA_K1_TL
+  const int need = (int)(sizeof(lopa::g_k1tl) / 8);
+  if (!out || n_words < need) return -need;
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, lopa::g_k1tl, sizeof(lopa::g_k1tl)) != cudaSuccess) return 0;
+  return need;
+#else
+  (void)out; (void)n_words;
+  return 0;
+#endif
+}
+
+// Debug (LOPA_LDG_TL builds): per-warp timeline of the warp-staged K1's last launch.
+extern "C" int lopa_debug_ldg_timeline(unsigned long long* out, int n_words) {
+#ifdef LOPA_LDG_TL
+  const int need = (int)(sizeof(lopa::g_ldg_tl) / 8);
+  if (!out || n_words < need) return -need;
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, lopa::g_ldg_tl, sizeof(lopa::g_ldg_tl)) != cudaSuccess) return 0;
+  return need;
+#else
+  (void)out; (void)n_words;
+  return 0;
+#endif
+}
+
+// Debug: resource attributes of the K1 kernel this build launches: {registers per thread,
+// max threads per block, static shared bytes, local bytes per thread, launch block size}.
+extern "C" int lopa_debug_k1_attrs(int32_t* out5) {
+  if (!out5) return LOPA_ERR_INVALID_ARG;
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, LOPA_K1_KERNEL);
+  if (e != cudaSuccess) return cuda_status(e);
+  out5[0] = fa.numRegs;
+  out5[1] = fa.maxThreadsPerBlock;
+  out5[2] = (int32_t)fa.sharedSizeBytes;
+  out5[3] = (int32_t)fa.localSizeBytes;
+  out5[4] = kK1Threads;
+  return LOPA_OK;
 }
 
 extern "C" const char* lopa_status_string(int status) {

@@ -43,7 +43,13 @@ bool carve_workspace(void* ws, size_t bytes, int32_t max_rows, int32_t vocab, Wo
 bool bind_device(void* stream, const void* ptr, int* device);
 int num_sms(int device);
 
-inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? LOPA_OK : LOPA_ERR_CUDA; }
+// Records the runtime's message of a failed call (lopa_last_cuda_error) and maps it to a status.
+void note_cuda_error(cudaError_t e);
+inline int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return LOPA_OK;
+  note_cuda_error(e);
+  return LOPA_ERR_CUDA;
+}
 
 int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, const void* records,
                      cudaStream_t s, const uint32_t* flags = nullptr, uint32_t epoch = 0);

@@ -39,6 +39,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
+#ifdef LOPA_MBAR_SPIN
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -73,6 +85,50 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "r"(smem_u32(p)));
   return v;
+}
+
+// Streaming 128-bit global load straight into registers: read-only path, no L1 allocation,
+// L2 eviction policy `pol` (evict-first for the logits: they are read exactly once).
+__device__ __forceinline__ uint4 ldg128_stream(const void* p, uint64_t pol) {
+  uint4 v;
+#if defined(LOPA_LDG_NOHINT)
+  (void)pol;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+#elif defined(LOPA_LDG_PLAIN)
+  (void)pol;
+  asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+#else
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+#endif
+  return v;
+}
+
+// ---- cp.async (LDGSTS): 16-byte global -> shared copies tracked in commit groups -----------
+__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src_gmem, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst_smem)),
+               "l"(src_gmem), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// Wait until at most N of this thread's most recent commit groups are pending.
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Global atomic add returning the old value, as one instruction: the compiler's warp
+// aggregation of atomicAdd (vote + shuffle of the returned value) would wait for the atomic's
+// round trip right at the call; here the value is waited for only where it is used.
+__device__ __forceinline__ uint32_t atom_add_u32(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 
 // L2-coherent loads for data written by other CTAs of the same launch.

@@ -62,6 +62,8 @@ class StepArgs(ctypes.Structure):
 _SIGS = {
     "lopa_version": (_i32, []),
     "lopa_status_string": (ctypes.c_char_p, [_i32]),
+    "lopa_last_cuda_error": (ctypes.c_char_p, []),
+    "lopa_debug_k1_attrs": (_i32, [ctypes.c_void_p]),
     "lopa_workspace_bytes": (_size, [_i32, _i32]),
     "lopa_num_segments": (_i32, [_i32]),
     "lopa_confidence": (_i32, [_c_void_p, _i64, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
@@ -94,6 +96,8 @@ _SIGS = {
     "lopa_bp_commit_winner": (_i32, [_c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p, _c_void_p]),
     "lopa_bp_destroy": (None, [_c_void_p]),
     "lopa_debug_timeline": (_i32, [_c_void_p, _i32]),
+    "lopa_debug_ldg_timeline": (_i32, [_c_void_p, _i32]),
+    "lopa_debug_k1_timeline": (_i32, [_c_void_p, _i32]),
     "lopa_profile_enable": (_i32, [_i32]),
     "lopa_profile_read": (_i32, [ctypes.POINTER(ctypes.c_float), _i32, ctypes.POINTER(_i32)]),
     "lopa_syn_generate": (_i32, [_u64, _i32, _i32, _i64, _i32, _i32, _c_void_p, _c_void_p, _i32,
@@ -128,6 +132,8 @@ def lib() -> ctypes.CDLL:
 def _check(st: int, what: str):
     if st != LOPA_OK:
         msg = lib().lopa_status_string(st).decode()
+        if st == 3:  # LOPA_ERR_CUDA: the runtime's own message
+            msg += ": " + lib().lopa_last_cuda_error().decode()
         raise LopaError(f"{what}: liblopa status {st} ({msg})")
 
 
