@@ -40,6 +40,11 @@ CONFIGS = {
     "dream-k15": dict(V=151936, W=32, k=15, tau=0.9, name="D2F-Dream verify step V=151936 W=32 k=15 tau=0.9 (configs[2] shape)"),
     "diffucoder": dict(V=151936, W=32, k=10, tau=0.95, name="D2F-DiffuCoder verify step V=151936 W=32 k=10 tau=0.95 (configs[3] shape)"),
 }
+# BASELINE configs[2] / configs[3]: whole Alg. 1 decode loops, branch-parallel at N > 1
+CONFIGS["dream-loop"] = dict(V=151936, W=32, k=15, tau=0.9, loop_blocks=8, seed=1,
+                             name="D2F-Dream full decode loop: 256-token generation (8 blocks of 32), k=15, tau=0.9, branch-parallel (configs[2])")
+CONFIGS["diffucoder-loop"] = dict(V=151936, W=32, k=10, tau=0.95, loop_blocks=4, seed=3,
+                                  name="D2F-DiffuCoder multi-block decode: 4 blocks of 32, k=10, tau=0.95, branch-parallel (configs[3])")
 # NEXT-4: the same step from the verify forward's hidden states (fused LM-head a1), Dream-7B
 # output projection K = 3584 (Qwen2.5-7B hidden size; outside the paper), one GPU
 CONFIGS["lmhead-dream"] = dict(V=151936, W=32, k=7, tau=0.9, K=3584,
@@ -225,6 +230,19 @@ def run_reference(args):
         return 0
     if CFG.get("K"):
         return run_reference_lmhead(args)
+    if CFG.get("loop_blocks"):
+        cb = cpu_baseline_loop(CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["seed"],
+                               budget_s=max(20.0, min(100.0, 2.0 * (args.steps + args.warmup))))
+        value = cb["value"]
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (SYN-D2F seeded logits; no weights)",
+                "config": {"workload": CFG["name"]}, "cpu_baseline": cb,
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "gpu_launches": 0}
+        print(json.dumps(line), flush=True)
+        return 0
     from oracle import lopa_oracle as O
     import syngen
     V, W, k, tau, seed = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["seed"]
@@ -555,45 +573,59 @@ def run_lopa(args):
                 "ms_per_block_incl_generator": l0.elapsed_time(l1) / 8,
                 "note": "one host read per iteration (branch count); SYN-D2F forward on the GPU"}
 
-    # e2e through the public API with HOST buffers: pinned logits -> device, step, results -> host
-    e2e = None
-    if world == 1:
-        host = full.cpu().pin_memory()
-        h_tok, h_msk, h_nb = tok.cpu().pin_memory(), msk.cpu().pin_memory(), nb.cpu().pin_memory()
-        d_log = torch.empty_like(full)
-        d_tok, d_msk, d_nb = torch.empty_like(tok), torch.empty_like(msk), torch.empty_like(nb)
-        o = st.out
-        h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory()
-                 for t in (o.winner, o.scores, o.next_tokens, o.next_mask, o.n_next, o.status)]
-        K2 = max(3, min(K, 50))
+    # e2e through the public API with HOST buffers: pinned logits -> device, step, results -> host.
+    # At N > 1 (branch-parallel) each rank copies its own shard of the logits (its branches'
+    # rows) and runs BranchParallel.step; the time is the max over ranks.
+    src = full if bp is None else bufs[0]
+    host = src.cpu().pin_memory()
+    h_tok, h_msk, h_nb = tok.cpu().pin_memory(), msk.cpu().pin_memory(), nb.cpu().pin_memory()
+    d_log = torch.empty_like(src)
+    d_tok, d_msk, d_nb = torch.empty_like(tok), torch.empty_like(msk), torch.empty_like(nb)
+    o = st.out
+    out_t = (o.winner, o.scores, o.next_tokens, o.next_mask, o.n_next, o.status)
+    h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in out_t]
+    K2 = max(3, min(K, 50))
 
-        def e2e_step():
-            d_log.copy_(host, non_blocking=True)
-            d_tok.copy_(h_tok, non_blocking=True)
-            d_msk.copy_(h_msk, non_blocking=True)
-            d_nb.copy_(h_nb, non_blocking=True)
+    def e2e_step():
+        d_log.copy_(host, non_blocking=True)
+        d_tok.copy_(h_tok, non_blocking=True)
+        d_msk.copy_(h_msk, non_blocking=True)
+        d_nb.copy_(h_nb, non_blocking=True)
+        if bp is None:
             st.step(d_log, d_nb, d_tok, d_msk, validate=False)
-            for h, t in zip(h_out, (o.winner, o.scores, o.next_tokens, o.next_mask, o.n_next, o.status)):
-                h.copy_(t, non_blocking=True)
+        else:
+            bp.step(d_log, d_nb, d_tok, d_msk)
+        for h, t in zip(h_out, out_t):
+            h.copy_(t, non_blocking=True)
 
-        for _ in range(3):
-            e2e_step()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(K2):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1)
-        h2d = full.numel() * 2 + tok.numel() * 4 + msk.numel() + nb.numel() * 4
-        d2h = sum(t.numel() * t.element_size() for t in h_out)
-        e2e = {"value": K2 / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": K2}
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K2):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    h2d = src.numel() * 2 + tok.numel() * 4 + msk.numel() + nb.numel() * 4
+    d2h = sum(t.numel() * t.element_size() for t in h_out)
+    e2e = {"value": K2 / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": K2}
+    if bp is not None:
+        e2e["note"] = "per rank: its logits shard (b_loc branches) + the replicated tables from pinned host memory; max over ranks"
 
     if rank == 0:
         cpu = cpu_all = None
-        if world == 1 and not args.no_cpu_baseline:
+        if not args.no_cpu_baseline:
+            # rank 0 only, on the whole step's workload (all ranks' branches): the CPU baseline
+            # of the same metric, independent of N
             cpu = cpu_baseline_oracle(full, tok, msk, nb, k, tau)
             cpu_all = cpu_baseline_all_cores(full, tok, msk, nb, k, tau)
         traffic = None
@@ -646,11 +678,239 @@ def run_lopa(args):
         if cpu_all is not None:
             line["cpu_baseline_all_cores"] = cpu_all
         print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()  # rank 0's CPU baseline runs while the others wait here
     if bp is not None:
         bp.close()
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+class _SingleGPU:
+    """decode_block_bp's driver interface over the fused single-GPU step (no exchange)."""
+
+    def __init__(self, st):
+        self.s = st
+        self.local = torch.zeros((st.max_branches, st.window, st.ld), dtype=torch.bfloat16, device=st.device)
+
+    def ranks(self):
+        return [(0, 0, self.s.max_branches, self.local)]
+
+    def step(self, *a):
+        if len(a) == 3:
+            a = (self.local, *a)
+        return self.s.step(*a, validate=False)
+
+
+def run_loop(args):
+    """BASELINE configs[2] / configs[3]: whole Alg. 1 decode loops over
+    `loop_blocks` sequential blocks (R22), branch-parallel over the N ranks at N > 1 (each
+    rank reduces only its own branches; one record all-gather per step).  A "step" = one verify
+    step of the loop (a block's initial predict counts as a step with one branch).  The SYN-D2F
+    logits of every step are generated once, by a recording pass of the same loop, and kept
+    resident in HBM -- each rank holds only its own branches' logits; the timed region replays
+    the loop from the start (one host read of the branch count per step, as lopa.decode_block)
+    until exactly K steps have run."""
+    from paper_2512_16229_b200 import lopa
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    V, W, k, tau, seed, nblk = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["seed"], CFG["loop_blocks"]
+    st = lopa.Stepper(V, W, k + 1, k, tau, dev)
+    use_bp = world > 1 or os.environ.get("LOPA_BENCH_FORCE_BP") == "1"
+    drv = lopa.BranchParallel(st, rank, world, p2p=os.environ.get("LOPA_BP_P2P") == "1") if use_bp else _SingleGPU(st)
+    _, lo, hi, _buf = drv.ranks()[0]
+    stream = torch.cuda.current_stream(dev)
+
+    # recording pass: the loop with the generator as the forward; each step's local logits kept
+    rec, fw_blocks, tokens = [], [], []
+    for blk in range(nblk):
+        steps = []
+        fwd = lambda t, m, out, blk=blk: lopa.syn_generate(seed, blk, V, t, m, out=out)
+        on_step = lambda out, n, t, m: steps.append((n, drv.local[: max(0, min(hi, n) - lo)].clone()))
+        t0 = torch.zeros(W, dtype=torch.int32, device=dev)
+        m0 = torch.ones(W, dtype=torch.uint8, device=dev)
+        tk, fw = lopa.decode_block_bp(drv, fwd, t0, m0, on_step=on_step)
+        rec.append(steps)
+        fw_blocks.append(fw)
+        tokens.append(tk)
+    torch.cuda.synchronize()
+    steps_per_pass = sum(fw_blocks)
+    tok = torch.zeros((k + 1, W), dtype=torch.int32, device=dev)
+    msk = torch.zeros((k + 1, W), dtype=torch.uint8, device=dev)
+    nb = torch.ones(1, dtype=torch.int32, device=dev)
+    lbuf = torch.zeros((drv.ranks()[0][3].shape), dtype=torch.bfloat16, device=dev)
+    # per step: this rank's logits rows, copied into the step's buffer view (zero copies: a view
+    # padded to b_loc rows is made once per recorded step)
+    padded = []
+    for steps in rec:
+        pb = []
+        for n, x in steps:
+            b = torch.zeros_like(lbuf)
+            if x.shape[0]:
+                b[: x.shape[0]] = x
+            pb.append(b)
+        padded.append(pb)
+    del rec
+    torch.cuda.synchronize()
+
+    def run_steps(count, check=True):
+        """Replay the recorded loop from block 0 for exactly `count` verify steps."""
+        done, blk, si = 0, 0, 0
+        while done < count:
+            if si == 0:
+                tok.zero_()
+                msk.zero_()
+                msk[0] = 1
+                nb.fill_(1)
+            out = drv.step(padded[blk][si], nb, tok, msk)
+            done += 1
+            n = int(out.n_next.item())
+            si += 1
+            if n == 0:
+                if check and si != fw_blocks[blk]:
+                    raise RuntimeError(f"replay diverged: block {blk} ended after {si} steps, recorded {fw_blocks[blk]}")
+                blk, si = (blk + 1) % nblk, 0
+            else:
+                tok.copy_(out.next_tokens)
+                msk.copy_(out.next_mask)
+                nb.copy_(out.n_next)
+
+    run_steps(max(args.warmup, 3))
+    torch.cuda.synchronize()
+    K = args.steps
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        run_steps(K)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    el_ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([el_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el_ms = float(t.item())
+    if int(st.out.status.item()) != 0:
+        raise lopa.LopaError(f"device status {int(st.out.status.item())}")
+    if use_bp:
+        drv.check()
+
+    # e2e: the same loop through the public API with each step's logits shard copied from pinned
+    # host memory (block 0, every step) and the step's results read back, inside the timed region
+    host0 = [b.cpu().pin_memory() for b in padded[0]]
+    o = st.out
+    h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory()
+             for t in (o.winner, o.next_tokens, o.next_mask, o.n_next, o.status)]
+    d_l = torch.empty_like(lbuf)
+
+    def e2e_block():
+        tok.zero_()
+        msk.zero_()
+        msk[0] = 1
+        nb.fill_(1)
+        for si, hb in enumerate(host0):
+            d_l.copy_(hb, non_blocking=True)
+            out = drv.step(d_l, nb, tok, msk)
+            for h, t in zip(h_out, (o.winner, o.next_tokens, o.next_mask, o.n_next, o.status)):
+                h.copy_(t, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            if int(h_out[3].item()) == 0:
+                return si + 1
+            tok.copy_(out.next_tokens)
+            msk.copy_(out.next_mask)
+            nb.copy_(out.n_next)
+        return len(host0)
+
+    e2e_block()
+    if dist:
+        dist.barrier()
+    reps = 3
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    n_e2e = sum(e2e_block() for _ in range(reps))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    h2d = sum(b.numel() * 2 for b in host0) / len(host0)
+    d2h = sum(t.numel() * t.element_size() for t in h_out)
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            cpu = cpu_baseline_loop(V, W, k, tau, seed)
+        tok_total = W * nblk
+        line = {
+            "metric": METRIC, "value": K / (el_ms / 1000.0), "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": el_ms / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (SYN-D2F seeded logits of each step, generated once and resident in HBM; transformer forward out of scope)",
+            "config": {"workload": CFG["name"], "blocks": nblk, "tokens_per_pass": tok_total,
+                       "verify_steps_per_pass": steps_per_pass, "forwards_per_block": fw_blocks,
+                       "tpf": tok_total / steps_per_pass,
+                       "parallelism": (f"bp{world}" + ("-p2p" if getattr(drv, "p2p", False) else "")) if use_bp else "single",
+                       "branches_this_rank": [lo, hi],
+                       "l2": "each step reads its own logits (resident, >= 4x L2 over a pass)"},
+            "tokens_per_s": tok_total * (K / steps_per_pass) / (el_ms / 1000.0),
+            "loop_note": "one host read (branch count) per step, as lopa.decode_block; the loop restarts at block 0 after the last block",
+            "clocks": clk.summary(),
+            "gpu_launches": K * (3 if use_bp else 2),
+            "e2e": {"value": n_e2e / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": n_e2e,
+                    "note": "block 0 replayed 3x: each step's logits shard (this rank's branches) from pinned host memory, results to host, max over ranks"},
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()  # rank 0's CPU baseline runs while the others wait here
+    if use_bp:
+        drv.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline_loop(V, W, k, tau, seed, budget_s=15.0):
+    """The oracle's Alg. 1 loop (NumPy fp64, one thread) on the same workload: whole blocks
+    (generator included, as the CPU stand-in for the forward) until ~budget_s."""
+    from oracle import lopa_oracle as O
+    from threadpoolctl import threadpool_limits
+    import syngen
+    steps, blocks, gen_s = 0, 0, 0.0
+    t0 = time.perf_counter()
+    with threadpool_limits(limits=1):
+        while time.perf_counter() - t0 < budget_s:
+            def fwd(t, m, blk=blocks):
+                nonlocal gen_s
+                g0 = time.perf_counter()
+                x = syngen.gen_logits(seed, blk, V, t, m)
+                gen_s += time.perf_counter() - g0
+                return x
+            tok0, msk0 = syngen.fresh_block(W)
+            steps += O.decode_block(fwd, tok0, msk0, k, tau).forwards
+            blocks += 1
+    el = time.perf_counter() - t0 - gen_s
+    return {"value": steps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{blocks} whole blocks ({steps} verify steps) of the loop, NumPy fp64 single thread; "
+                      f"the generator's time ({gen_s:.1f} s) excluded"}
 
 
 def run_lmhead(args):
@@ -825,9 +1085,27 @@ def main():
     ap.add_argument("--impl", default="lopa", choices=["lopa", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="dream", choices=sorted(CONFIGS))
+    # overrides of the selected config (SPEC.md:493's --k/--W/--V/--tau/--seed)
+    ap.add_argument("--k", type=int, default=None, help="lookahead branches")
+    ap.add_argument("--W", type=int, default=None, help="window (block) length")
+    ap.add_argument("--V", type=int, default=None, help="vocabulary size")
+    ap.add_argument("--tau", type=float, default=None, help="Eq. 1 threshold")
+    ap.add_argument("--seed", type=int, default=None, help="SYN-D2F seed")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     CFG.update(V=c["V"], W=c["W"], k=c["k"], tau=c["tau"], name=c["name"])
+    CFG["loop_blocks"] = c.get("loop_blocks")
+    if c.get("seed") is not None:
+        CFG["seed"] = c["seed"]
+    for key in ("k", "tau", "seed"):
+        if getattr(args, key) is not None:
+            CFG[key] = getattr(args, key)
+    if args.V is not None:
+        CFG["V"] = args.V
+    if args.W is not None:
+        CFG["W"] = args.W
+    if any(getattr(args, x) is not None for x in ("k", "tau", "seed", "V", "W")):
+        CFG["name"] += f" [overridden: V={CFG['V']} W={CFG['W']} k={CFG['k']} tau={CFG['tau']} seed={CFG['seed']}]"
     if args.warmup < 3:
         args.warmup = 3
     CFG["K"] = c.get("K")
@@ -835,6 +1113,8 @@ def main():
         return run_reference(args)
     if CFG["K"]:
         return run_lmhead(args)
+    if CFG["loop_blocks"]:
+        return run_loop(args)
     return run_lopa(args)
 
 

@@ -531,6 +531,7 @@ class BranchParallel:
         self.conf = torch.full((self.b_loc, W), float("nan"), dtype=torch.float32, device=d)
         self.argmax = torch.full((self.b_loc, W), -1, dtype=torch.int32, device=d)
         self.scores = torch.empty(world * self.b_loc, dtype=torch.float32, device=d)
+        self.local = None  # this rank's logits buffer for decode_block_bp (allocated on first use)
         self.p2p = p2p
         self._payload_bytes = payload_bytes
         if p2p:
@@ -545,8 +546,21 @@ class BranchParallel:
             raw_all = (ctypes.c_uint8 * (IPC_HANDLE_BYTES * world))(*b"".join(allh))
             _check(lib().lopa_bp_p2p_open(self.h, raw_all), "lopa_bp_p2p_open")
 
-    def step(self, local_logits, n_branches, branch_tokens, branch_mask) -> StepOutputs:
-        """local_logits: this rank's bf16 [b_loc][W][ld]; tables are the full replicated ones."""
+    def ranks(self):
+        """(rank, lo, hi, local logits buffer [b_loc][W][ld]) of this process's rank."""
+        if self.local is None:
+            self.local = torch.zeros((self.b_loc, self.s.window, self.s.ld), dtype=torch.bfloat16,
+                                     device=self.s.device)
+        return [(self.rank, self.lo, self.hi, self.local)]
+
+    def step(self, *a) -> StepOutputs:
+        """step(local_logits, n_branches, branch_tokens, branch_mask), or step(n_branches,
+        branch_tokens, branch_mask) on the buffer of ranks().  local_logits: this rank's bf16
+        [b_loc][W][ld]; the tables are the full replicated ones."""
+        if len(a) == 3:
+            self.ranks()
+            a = (self.local, *a)
+        local_logits, n_branches, branch_tokens, branch_mask = a
         s = self.s
         a = s.args(local_logits, n_branches, branch_tokens, branch_mask)
         a.conf, a.argmax = self.conf.data_ptr(), self.argmax.data_ptr()
@@ -613,34 +627,98 @@ class BranchParallel:
             self.h = None
 
 
+class BPEmulator:
+    """Single-GPU stand-in for ``world`` BranchParallel ranks (tests, and the bench's
+    LOPA_BENCH_EMULATE_BP): every rank's local half (a1 + local a2 + its record,
+    lopa_bp_local) runs on that rank's own logits buffer, then the global half (lopa_bp_finish)
+    on the record array.  The NCCL all-gather is replaced by each rank writing its record in
+    place into one contiguous array -- exactly the all-gather's result.  Same kernels as
+    BranchParallel.step."""
+
+    def __init__(self, stepper: Stepper, world: int):
+        self.s, self.world = stepper, world
+        W, d = stepper.window, stepper.device
+        self.b_loc = bp_shard(stepper.max_branches, world, 0)[0]
+        self.rb = record_bytes(W, self.b_loc)
+        self.records = torch.zeros(world * self.rb, dtype=torch.uint8, device=d)
+        self.scores = torch.empty(world * self.b_loc, dtype=torch.float32, device=d)
+        self.ws = [new_workspace(self.b_loc * W, stepper.vocab, d) for _ in range(world)]
+        self.conf = [torch.full((self.b_loc, W), float("nan"), dtype=torch.float32, device=d)
+                     for _ in range(world)]
+        self.argmax = [torch.full((self.b_loc, W), -1, dtype=torch.int32, device=d) for _ in range(world)]
+        self.local = [torch.zeros((self.b_loc, W, stepper.ld), dtype=torch.bfloat16, device=d)
+                      for _ in range(world)]
+
+    def ranks(self):
+        """(rank, lo, hi, local logits buffer) of every emulated rank."""
+        return [(r, *bp_shard(self.s.max_branches, self.world, r)[1:], self.local[r])
+                for r in range(self.world)]
+
+    def step(self, n_branches, branch_tokens, branch_mask) -> StepOutputs:
+        """One BP step on the ranks' local buffers (self.local[r] holds rank r's branches)."""
+        st, d = self.s, self.s.device
+        for r in range(self.world):
+            a = st.args(self.local[r], n_branches, branch_tokens, branch_mask)
+            a.conf, a.argmax = self.conf[r].data_ptr(), self.argmax[r].data_ptr()
+            a.workspace, a.workspace_bytes = self.ws[r].data_ptr(), self.ws[r].numel()
+            a.scores = self.scores.data_ptr()
+            _check(lib().lopa_bp_local(ctypes.byref(a), r * self.b_loc, self.b_loc,
+                                       ctypes.c_void_p(self.records.data_ptr() + r * self.rb), _stream(d)),
+                   "lopa_bp_local")
+        a = st.args(self.local[0], n_branches, branch_tokens, branch_mask)
+        a.scores = self.scores.data_ptr()
+        _check(lib().lopa_bp_finish(ctypes.byref(a), self.b_loc, self.world, _p(self.records), _stream(d)),
+               "lopa_bp_finish")
+        return st.out
+
+    def gathered(self):
+        """conf / argmax of every global branch [max_branches][W] (rank r's local branch jl is
+        global branch r * b_loc + jl)."""
+        mb = self.s.max_branches
+        conf = torch.cat(self.conf)[:mb]
+        amax = torch.cat(self.argmax)[:mb]
+        return conf, amax
+
+
 def bp_emulate_step(stepper: Stepper, world: int, logits, n_branches, branch_tokens, branch_mask):
-    """Single-GPU emulation of a `world`-rank BP step: each rank's local half runs on its slice
-    of the logits and writes its record in place, then the global half runs.  Exercises the same
-    kernels as BranchParallel.step minus the NCCL all-gather (whose effect is the identity on
-    the contiguous record array).  Returns (outputs, per-rank local conf list, scores)."""
-    W, d = stepper.window, stepper.device
-    b_loc, _, _ = bp_shard(stepper.max_branches, world, 0)
-    rb = record_bytes(W, b_loc)
-    records = torch.zeros(world * rb, dtype=torch.uint8, device=d)
-    scores = torch.empty(world * b_loc, dtype=torch.float32, device=d)
-    confs = []
-    for r in range(world):
-        _, lo, hi = bp_shard(stepper.max_branches, world, r)
-        local = torch.zeros((b_loc, W, logits.shape[-1]), dtype=logits.dtype, device=d)
+    """One emulated `world`-rank BP step on full logits [max_branches][W][ld] (each rank gets
+    its slice).  Returns (outputs, per-rank (conf, argmax) list, scores)."""
+    emu = BPEmulator(stepper, world)
+    for r, lo, hi, buf in emu.ranks():
         if hi > lo:
-            local[: hi - lo] = logits[lo:hi]
-        ws = new_workspace(b_loc * W, stepper.vocab, d)
-        conf = torch.full((b_loc, W), float("nan"), dtype=torch.float32, device=d)
-        amax = torch.full((b_loc, W), -1, dtype=torch.int32, device=d)
-        a = stepper.args(local, n_branches, branch_tokens, branch_mask)
-        a.conf, a.argmax, a.workspace, a.workspace_bytes = conf.data_ptr(), amax.data_ptr(), ws.data_ptr(), ws.numel()
-        a.scores = scores.data_ptr()
-        _check(lib().lopa_bp_local(ctypes.byref(a), r * b_loc, b_loc,
-                                   ctypes.c_void_p(records.data_ptr() + r * rb), _stream(d)),
-               "lopa_bp_local")
-        confs.append((conf, amax))
-    a = stepper.args(logits, n_branches, branch_tokens, branch_mask)
-    a.scores = scores.data_ptr()
-    _check(lib().lopa_bp_finish(ctypes.byref(a), b_loc, world, _p(records), _stream(d)),
-           "lopa_bp_finish")
-    return stepper.out, confs, scores
+            buf[: hi - lo] = logits[lo:hi]
+    out = emu.step(n_branches, branch_tokens, branch_mask)
+    return out, list(zip(emu.conf, emu.argmax)), emu.scores
+
+
+def decode_block_bp(bp, forward, tokens0: torch.Tensor, mask0: torch.Tensor,
+                    max_forwards: int | None = None, on_step=None):
+    """Alg. 1 over one window, branch-parallel (P:154-180 with BP): the branch tables are
+    replicated; each rank runs the forward of ITS OWN present branches only (global branches
+    [lo, min(hi, n)), into its local logits buffer) and reduces them, and the exchange selects the
+    global winner.  ``bp`` is a BranchParallel (this process's rank) or a BPEmulator (every rank
+    on one GPU).  ``forward(branch_tokens[m][W], branch_mask[m][W], out=logits[m][W][ld])`` as in
+    decode_block.  ``on_step(outputs, n_branches_before)`` is called after every step (tests).
+    Returns (tokens int32 [W] on the device, forwards); one host read per iteration."""
+    st = bp.s
+    k, W, dev = st.k, st.window, st.device
+    tok = torch.zeros((k + 1, W), dtype=torch.int32, device=dev)
+    msk = torch.zeros((k + 1, W), dtype=torch.uint8, device=dev)
+    tok[0], msk[0] = tokens0.to(torch.int32), _u8(mask0)
+    nb = torch.ones(1, dtype=torch.int32, device=dev)
+    forwards, n = 0, 1
+    while True:
+        for _, lo, hi, buf in bp.ranks():
+            m = max(0, min(hi, n) - lo)
+            if m > 0:
+                forward(tok[lo:lo + m], msk[lo:lo + m], out=buf[:m])
+        out = bp.step(nb, tok, msk)
+        forwards += 1
+        if on_step is not None:
+            on_step(out, n, tok, msk)
+        n = int(out.n_next.item())
+        if n == 0 or (max_forwards is not None and forwards >= max_forwards):
+            return out.next_tokens[0].clone(), forwards
+        tok.copy_(out.next_tokens)
+        msk.copy_(out.next_mask)
+        nb.copy_(out.n_next)
