@@ -90,6 +90,10 @@ const char* lopa_last_cuda_error(void);
 /* Debug: {registers/thread, max threads/block, static shared bytes, local bytes/thread, block
  * size launched} of the vocabulary-reduction kernel K1 this build uses. */
 int lopa_debug_k1_attrs(int32_t* out5);
+/* Debug, checked builds (-DLOPA_CHECKED, the library's own bounds / protocol checks): writes
+ * {violations, first violating site, bitmask of violating sites} counted since the last call and
+ * resets them.  Returns LOPA_ERR_UNSUPPORTED (zeros written) in product builds. */
+int lopa_debug_check_read(uint32_t* out3);
 
 /* Bytes of device workspace needed for up to max_rows rows of `vocab` logits. */
 size_t lopa_workspace_bytes(int32_t max_rows, int32_t vocab);

@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include <cuda_bf16.h>
@@ -74,6 +75,27 @@ __device__ __forceinline__ void tl_clk_dep(int slot, float dep) {
 #define TL(slot) ((void)0)
 #define TLMAX(slot) ((void)0)
 #define TLC(slot) ((void)0)
+#endif
+// Checked builds (-DLOPA_CHECKED, the library's own sanitizer tier: compute-sanitizer is not
+// available on this pool): every global access of the step's kernels is tested against the
+// bounds the C ABI's contract implies (liblopa.h), K1's stage ring asserts that a consumer reads
+// the stage use it waited for, and K2 / the fold kernel assert that every partial they fold was
+// written by THIS launch's K1 (a per-launch epoch stamped into the partial's unused 4th word).
+// Violations are counted in device globals read by lopa_debug_check_read().
+#ifdef LOPA_CHECKED
+__device__ unsigned int g_chk_count;
+__device__ unsigned int g_chk_first;
+__device__ unsigned int g_chk_sites;
+__device__ __noinline__ void chk_fail(int site) {
+  if (atomicAdd(&g_chk_count, 1u) == 0) g_chk_first = (unsigned)site;
+  atomicOr(&g_chk_sites, 1u << (site & 31));
+}
+#define LOPA_CHK(cond, site) \
+  do {                       \
+    if (!(cond)) chk_fail(site); \
+  } while (0)
+#else
+#define LOPA_CHK(cond, site) ((void)0)
 #endif
 }  // namespace lopa
 #include "lopa_decide.cuh"
@@ -123,6 +145,8 @@ struct Params {
   int32_t window;
   int32_t branch_base;         // global id of logits branch 0 (BP local)
   int32_t cap;                 // branch capacity of the logits / conf tables
+  int32_t table_rows;          // rows of the replicated branch tables (max_branches; n_rows / 1 for a1 alone)
+  uint32_t epoch;              // checked builds: per-launch stamp of K1's partials (0 otherwise)
   float* conf;
   int32_t* argmax;
   int32_t* dev_status;
@@ -455,6 +479,16 @@ __device__ __forceinline__ FoldAcc fold_tree16(int n, const float4 (&q)[16]) {
   return FoldAcc{M, t[0], a};
 }
 
+// The 4th word of a group partial: the launch's epoch in checked builds, +0 otherwise.
+__device__ __forceinline__ float part_stamp(const Params& P) {
+#ifdef LOPA_CHECKED
+  return __uint_as_float(P.epoch);
+#else
+  (void)P;
+  return 0.f;
+#endif
+}
+
 // ------------------------------------------------------------------ K2's decision tail
 // Everything the decision tail needs, staged in K2's shared memory.
 constexpr int kScoreWarps = 8;  // warps scoring branches in the tail
@@ -580,6 +614,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
     for (int q = 0; q < kPos; ++q) cnt += (T.keys[q] > mine) ? 1 : 0;
     const int rk = T.b0_msk[pos] ? cnt : (1 << 20);
     T.rank[pos] = rk;
+    LOPA_CHK(rk >= nl || rk < P.k, 8);
     if (rk < nl && P.lookahead) P.lookahead[rk] = pos;
     if (P.lookahead)
       for (int q = nl + tid; q < P.k; q += kPos) P.lookahead[q] = -1;
@@ -594,6 +629,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
     const int rk = T.rank[i];
     for (int j = 0; j <= nl; ++j) {
       const bool fill = (j >= 1) && (rk == j - 1);
+      LOPA_CHK(j <= P.k && i < W, 8);
       P.next_tokens[(size_t)j * W + i] = fill ? ta : tb;
       P.next_mask[(size_t)j * W + i] = fill ? (uint8_t)0 : mb;
     }
@@ -672,6 +708,9 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   uint32_t* icnt = reinterpret_cast<uint32_t*>(ipart + kItemSlots * kPartPerItem);
   uint32_t* gbits = icnt + kItemSlots;
   uint16_t* vlist = reinterpret_cast<uint16_t*>(gbits + 2 * kMaxGroups);  // [LOPA_MAX_ROWS]
+#ifdef LOPA_CHECKED
+  uint32_t* stage_seq = reinterpret_cast<uint32_t*>(vlist + LOPA_MAX_ROWS);  // [kStages]
+#endif
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) TL(0);
@@ -714,9 +753,13 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     if (i >= (uint32_t)kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
     if (i < 48) K1TL(2 * i + 1);
     stage_info[s] = make_int4(row, g, slot, s1 - s0);
+#ifdef LOPA_CHECKED
+    stage_seq[s] = i;
+#endif
     const int e0 = s0 * P.seg_len;
     const int e1 = min(P.vocab, s1 * P.seg_len);
     const uint32_t bytes = (uint32_t)(((e1 - e0 + 7) >> 3) << 4);
+    LOPA_CHK(row >= 0 && row < P.n_cand && g >= 0 && g < n_grp && (int64_t)e0 + bytes / 2 <= P.ld, 1);
     mbar_arrive_expect_tx(&full[s], bytes);
     bulk_g2s(stages + (size_t)s * kStageBytes, P.logits + (size_t)row * P.ld + e0, bytes,
              &full[s], pol);
@@ -749,7 +792,10 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     // r / W < nb_eff (no division); the mask byte is read only for rows of present branches,
     // so a rank whose shard runs past the table's last branch never reads beyond it
     bool v = in && (!P.n_branches || (int64_t)r < (int64_t)nb_eff * W);
-    if (v && P.row_mask) v = P.row_mask[r] != 0;
+    if (v && P.row_mask) {
+      LOPA_CHK((int64_t)P.branch_base * W + r < (int64_t)P.table_rows * W, 2);
+      v = P.row_mask[r] != 0;
+    }
     const uint32_t bits = __ballot_sync(0xffffffffu, v);
     if (lane == 0) gbits[g] = bits;
   }
@@ -862,6 +908,9 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
         if (c == 0) TL(14);
         if (i >= (uint32_t)kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
         stage_info[s] = make_int4(-1, 0, 0, 0);
+#ifdef LOPA_CHECKED
+        stage_seq[s] = i;
+#endif
         mbar_arrive(&full[s]);
       }
     }
@@ -884,6 +933,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
       if (first && warp == 1 && lane == 0) TL(2);
       first = false;
       const int4 info = stage_info[s];
+      LOPA_CHK(stage_seq[s] == i, 4);  // the stage use this warpgroup waited for, not a refill
       if (info.x < 0) break;
       const int row = info.x, g = info.y, slot = info.z, nsi = info.w;
       if (jseg >= nsi || !row_valid(row)) {  // short item, or a speculative copy of a skipped row
@@ -912,7 +962,8 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
           __threadfence_block();
           const float4* q = ipart + slot * kPartPerItem;
           const FoldAcc f = fold_seq(kWarpsPerSeg * nsi, [&](int p) { return q[p]; });
-          P.gpart[(size_t)g * P.n_cand + row] = make_float4(f.M, f.S, __uint_as_float(f.a), 0.f);
+          LOPA_CHK(g >= 0 && g < P.n_grp && row >= 0 && row < P.n_cand, 3);
+          P.gpart[(size_t)g * P.n_cand + row] = make_float4(f.M, f.S, __uint_as_float(f.a), part_stamp(P));
           icnt[slot] = 0;
           mbar_arrive(&slot_free[slot]);
         }
@@ -1156,7 +1207,10 @@ __global__ void __launch_bounds__(kLThreads, 1) lopa_reduce_ldg_kernel(const Par
     const int nb_eff = P.n_branches ? *P.n_branches - P.branch_base : 0x7FFFFFFF;
     // the mask byte is read only for rows of present branches (r / W < nb_eff)
     bool v = in && (!P.n_branches || (int64_t)r < (int64_t)nb_eff * W);
-    if (v && P.row_mask) v = P.row_mask[r] != 0;
+    if (v && P.row_mask) {
+      LOPA_CHK((int64_t)P.branch_base * W + r < (int64_t)P.table_rows * W, 2);
+      v = P.row_mask[r] != 0;
+    }
     const uint32_t bits = __ballot_sync(0xffffffffu, v);
     if (lane == 0) gbits[gq] = bits;
   }
@@ -1401,6 +1455,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
 #pragma unroll
   for (int u = 0; u < kRowsPerThread; ++u) {
     const int idx = kRowsPerThread * tid + u;
+    if (idx < nt) LOPA_CHK((int64_t)P.branch_base * W + idx < (int64_t)P.table_rows * W, 5);
     const uint8_t mk = idx < nt ? bmask[idx] : (uint8_t)0;
     if (idx < nt) {
       T.msk[idx] = mk;
@@ -1484,6 +1539,10 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
         float4 qr[16];
 #pragma unroll
         for (int p = 0; p < 16; ++p) qr[p] = gst[row + p * stride];
+#ifdef LOPA_CHECKED
+        for (int p = 0; p < n_grp; ++p) LOPA_CHK(__float_as_uint(qr[p].w) == P.epoch, 6);
+        LOPA_CHK(row < P.n_cand, 7);
+#endif
         const FoldAcc f = fold_tree16(16, qr);
 #ifdef LOPA_TIMELINE
         if (rc == 0) tl_clk_dep(17, f.S);
@@ -1502,6 +1561,10 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
         tl_clk_dep(21, q0.x);  // one staged partial read back
       }
 #endif
+#ifdef LOPA_CHECKED
+      for (int p = 0; p < n_grp; ++p) LOPA_CHK(__float_as_uint(gst[row + p * P.n_cand].w) == P.epoch, 6);
+      LOPA_CHK(row < P.n_cand, 7);
+#endif
       const FoldAcc f = fold_row_smem(gst + row, n_grp, P.n_cand);
 #ifdef LOPA_TIMELINE
       if (rc == 0) tl_clk_dep(17, f.S);
@@ -1519,6 +1582,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   } else
   for (int rc = tid; rc < n_masked; rc += kTailThreads) {
     const int row = rows[rc];
+#ifdef LOPA_CHECKED
+    for (int p = 0; p < n_grp; ++p)
+      LOPA_CHK(__float_as_uint(__ldcg(P.gpart + row + (size_t)p * P.n_cand).w) == P.epoch, 6);
+    LOPA_CHK(row < P.n_cand, 7);
+#endif
     const FoldAcc f = fold_row_global(P.gpart + row, n_grp, (size_t)P.n_cand);
     const float c = __fdiv_rn(1.0f, f.S);
     P.conf[row] = c;
@@ -1578,8 +1646,16 @@ __global__ void __launch_bounds__(kFoldRows) lopa_fold_kernel(const Params P) {
     float4 qr[16];
 #pragma unroll
     for (int p = 0; p < 16; ++p) qr[p] = st[p * kFoldRows + threadIdx.x];
+#ifdef LOPA_CHECKED
+    if (valid)
+      for (int p = 0; p < P.n_grp; ++p) LOPA_CHK(__float_as_uint(qr[p].w) == P.epoch, 10);
+#endif
     f = fold_tree16(16, qr);
   } else if (valid) {
+#ifdef LOPA_CHECKED
+    for (int p = 0; p < P.n_grp; ++p)
+      LOPA_CHK(__float_as_uint(__ldcg(P.gpart + r + (size_t)p * P.n_cand).w) == P.epoch, 10);
+#endif
     f = fold_row_global(P.gpart + r, P.n_grp, (size_t)P.n_cand);
   }
   if (valid) {
@@ -1594,7 +1670,11 @@ static_assert(LOPA_MAX_ROWS % kTailThreads == 0, "rows per tail thread");
 
 constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + (2 * kStages + kItemSlots) * 8 +
                               kStages * 16 + kItemSlots * kPartPerItem * 16 + kItemSlots * 4 +
-                              2 * kMaxGroups * 4 + kVlistBytes + 16;
+                              2 * kMaxGroups * 4 + kVlistBytes + 16
+#ifdef LOPA_CHECKED
+                              + kStages * 4
+#endif
+    ;
 
 // ------------------------------------------------------------------ small decision kernels
 template <int S>
@@ -1695,8 +1775,10 @@ __global__ void bp_finish_kernel(const Params P, const uint8_t* records, int wor
     float v = -INFINITY;
     if (r < world) {
       RecordView rv = record_view(const_cast<uint8_t*>(records) + rb * r, b_loc);
+      LOPA_CHK(*rv.n_present <= b_loc && *rv.b_loc == b_loc, 9);
       if (jl < *rv.n_present) v = rv.scores[jl];
     }
+    LOPA_CHK(j < P.table_rows, 9);
     P.scores[j] = v;
   }
   const int W = P.window;
@@ -1895,9 +1977,14 @@ constexpr size_t kK1Smem = kSmemBytes;
 constexpr int kK1CtasPerSm = LOPA_CTAS_PER_SM;
 #endif
 
-static int launch_reduce(const Params& P, int device, cudaStream_t s, bool k1_only = false) {
+static int launch_reduce(const Params& P0, int device, cudaStream_t s, bool k1_only = false) {
   int st = ensure_kernel_attrs(device);
   if (st != LOPA_OK) return st;
+  Params P = P0;
+#ifdef LOPA_CHECKED
+  static std::atomic<uint32_t> g_epoch{0};
+  P.epoch = 1u + (g_epoch.fetch_add(1u) & 0x3FFFFFFFu);  // never 0: a zeroed workspace never matches
+#endif
   if (k1_only) {  // measurement: K1 alone, in the step's launch configuration
     const int g = kK1CtasPerSm * (num_sms(device) - 1);
     return cuda_status(launch_pdl(LOPA_K1_KERNEL, dim3(g), dim3(kK1Threads), kK1Smem, s, P));
@@ -1964,6 +2051,7 @@ static Params base_params(const lopa_step_args_t* a, const Workspace& ws) {
   segmentation(a->vocab, &P.n_seg, &P.seg_len);
   P.n_grp = num_groups(P.n_seg);
   P.window = a->window;
+  P.table_rows = a->max_branches;
   P.n_branches = a->n_branches;
   P.conf = a->conf;
   P.argmax = a->argmax;
@@ -2159,6 +2247,31 @@ extern "C" int lopa_debug_ldg_timeline(unsigned long long* out, int n_words) {
 #endif
 }
 
+// Checked builds: {violations, first violating site, bitmask of sites} since the last read, then
+// reset.  LOPA_ERR_UNSUPPORTED in product builds.
+extern "C" int lopa_debug_check_read(uint32_t* out3) {
+  if (!out3) return LOPA_ERR_INVALID_ARG;
+#ifdef LOPA_CHECKED
+  cudaDeviceSynchronize();
+  unsigned v[3] = {0, 0, 0};
+  if (cudaMemcpyFromSymbol(&v[0], lopa::g_chk_count, 4) != cudaSuccess ||
+      cudaMemcpyFromSymbol(&v[1], lopa::g_chk_first, 4) != cudaSuccess ||
+      cudaMemcpyFromSymbol(&v[2], lopa::g_chk_sites, 4) != cudaSuccess)
+    return LOPA_ERR_CUDA;
+  const unsigned z = 0;
+  cudaMemcpyToSymbol(lopa::g_chk_count, &z, 4);
+  cudaMemcpyToSymbol(lopa::g_chk_first, &z, 4);
+  cudaMemcpyToSymbol(lopa::g_chk_sites, &z, 4);
+  out3[0] = v[0];
+  out3[1] = v[1];
+  out3[2] = v[2];
+  return LOPA_OK;
+#else
+  out3[0] = out3[1] = out3[2] = 0;
+  return LOPA_ERR_UNSUPPORTED;
+#endif
+}
+
 // Debug: resource attributes of the K1 kernel this build launches: {registers per thread,
 // max threads per block, static shared bytes, local bytes per thread, launch block size}.
 extern "C" int lopa_debug_k1_attrs(int32_t* out5) {
@@ -2242,6 +2355,7 @@ static int confidence_impl(const void* logits, int64_t ld, int32_t n_rows, int32
   P.n_cand = n_rows;
   P.row_mask = row_mask;
   P.window = 1;
+  P.table_rows = n_rows;
   P.conf = conf;
   P.argmax = argmax;
   P.dev_status = dev_status;

@@ -64,6 +64,7 @@ _SIGS = {
     "lopa_status_string": (ctypes.c_char_p, [_i32]),
     "lopa_last_cuda_error": (ctypes.c_char_p, []),
     "lopa_debug_k1_attrs": (_i32, [ctypes.c_void_p]),
+    "lopa_debug_check_read": (_i32, [ctypes.c_void_p]),
     "lopa_workspace_bytes": (_size, [_i32, _i32]),
     "lopa_num_segments": (_i32, [_i32]),
     "lopa_confidence": (_i32, [_c_void_p, _i64, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
