@@ -179,6 +179,51 @@ def cpu_baseline_oracle(full, tok, msk, nb, k, tau, budget_s=12.0):
                       f"in {el:.1f} s, NumPy fp64 single thread"}
 
 
+def oracle_step_report(full, tok, msk, nb, k, tau, out, bp_conf=None):
+    """The bench step's inputs through the oracle once (rank 0): near-tie counts of the step's
+    decisions (R16: governing gap < 1e-6, SURVEY §8(d) "near-tie count") and the GPU step's
+    agreement with the oracle on exactly the timed inputs (conf max |err|, argmax, winner, the
+    spawned tables)."""
+    from oracle import lopa_oracle as O
+    n = int(nb.item())
+    L16 = full.view(torch.int16).cpu().numpy().view(np.uint16)[:n]
+    t_np, m_np = tok.cpu().numpy()[:n], msk.cpu().numpy()[:n]
+    r = O.step(L16, t_np, m_np, k, tau)
+    sel = m_np.astype(bool)
+    near = {"select": 0, "anchor": 0, "fallback": 0, "spawn": 0}
+    gaps = {}
+    sc = sorted([x for x in r.scores if np.isfinite(x)], reverse=True)
+    gaps["select"] = float(sc[0] - sc[1]) if len(sc) > 1 else None
+    cw = r.conf[r.winner]
+    Mw = [i for i in range(m_np.shape[1]) if m_np[r.winner, i]]
+    if Mw:
+        gaps["anchor"] = float(min(abs(float(cw[i]) - float(np.float32(tau))) for i in Mw))
+        c = sorted((float(cw[i]) for i in Mw), reverse=True)
+        gaps["fallback"] = float(c[0] - c[1]) if len(c) > 1 else None
+    if not r.done:
+        M0 = [i for i in range(m_np.shape[1]) if r.anchor.mask[i]]
+        c = sorted((float(cw[i]) for i in M0), reverse=True)[: k + 1]
+        gaps["spawn"] = float(min((c[q] - c[q + 1] for q in range(len(c) - 1)), default=float("inf")))
+    for key, g in gaps.items():
+        if g is not None and g < 1e-6:
+            near[key] += 1
+    rep = {"near_ties": near, "min_gaps": gaps}
+    g_w = int(out.winner.item())
+    par = {"winner_equal": g_w == r.winner}
+    if bp_conf is None:
+        gc = out.conf.cpu().numpy()[:n].astype(np.float64)
+        ga = out.argmax.cpu().numpy()[:n]
+        par["conf_max_abs_err"] = float(np.abs(gc[sel] - r.conf[sel]).max())
+        par["argmax_equal"] = bool(np.array_equal(ga[sel], r.argmax[sel]))
+    if not r.done:
+        nn = int(out.n_next.item())
+        par["spawn_equal"] = bool(nn == len(r.spawn.lookahead) + 1 and
+                                  np.array_equal(out.next_tokens.cpu().numpy()[:nn], r.spawn.tokens) and
+                                  np.array_equal(out.next_mask.cpu().numpy()[:nn], r.spawn.mask))
+    rep["oracle_parity"] = par
+    return rep
+
+
 def cpu_baseline_all_cores(full, tok, msk, nb, k, tau, budget_s=8.0):
     """The same oracle step with its row reductions spread over every host core (threads;
     NumPy releases the GIL inside the vectorised exp / sum), as SURVEY §8(d) asks next to the
@@ -465,22 +510,32 @@ def run_lopa(args):
         bp.check()
     value = K / (el_ms / 1000.0)
     pair_ms = statistics.mean(per) if per else float("nan")
-    # step-time distribution: the same steps in 20 batches, CUDA events at the
-    # batch ends only; per-batch mean step time -> p10 / p50 / p90
-    nbatch = 20
-    per_b = max(1, K // nbatch)
-    bt = []
-    head_start(stream)
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(nbatch + 1)]
-    evs[0].record(stream)
-    for b_ in range(nbatch):
-        for i in range(b_ * per_b, (b_ + 1) * per_b):
+    # step-time distribution: N_LAT individually timed steps, each bracketed by its
+    # own CUDA event pair on the stream (queued behind a device-side head start, so host launch
+    # time never falls inside a pair).  The events sit between consecutive steps, so each step
+    # runs ISOLATED: K1's launch cannot overlap the previous step's tail as in the PDL-chained
+    # timed region (whose mean is the headline).  Percentiles over the per-step latencies.
+    N_LAT = max(1000, min(K, 2000))
+    lat_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(N_LAT)]
+    lat = []
+    for b0 in range(0, N_LAT, 250):
+        head_start(stream)
+        for i in range(b0, min(N_LAT, b0 + 250)):
+            lat_ev[i][0].record(stream)
             launch(i)
-        evs[b_ + 1].record(stream)
-    torch.cuda.synchronize()
-    bt = sorted(evs[b_].elapsed_time(evs[b_ + 1]) * 1000.0 / per_b for b_ in range(nbatch))
-    step_dist = {"p10_us": bt[1], "p50_us": bt[nbatch // 2], "p90_us": bt[-2], "batches": nbatch,
-                 "steps_per_batch": per_b}
+            lat_ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    lat = sorted(a.elapsed_time(b) * 1000.0 for a, b in lat_ev)
+
+    def pct(q):
+        return lat[min(len(lat) - 1, int(q * (len(lat) - 1) + 0.5))]
+
+    step_dist = {"isolated_step_us": {"p10": pct(0.10), "p50": pct(0.50), "p90": pct(0.90),
+                                      "p99": pct(0.99), "min": lat[0], "max": lat[-1], "n": len(lat)},
+                 "chained_mean_us": el_ms / K * 1000.0,
+                 "note": "isolated: one event pair per step (no PDL overlap with the neighbouring "
+                         "steps); chained: the headline's mean over K back-to-back steps"}
     # dense kernel roofline (SURVEY §8(d) mode (i)): every (branch, position) row of the
     # buffers reduced, (k + 1) * W rows, same CUDA-event chain as pass A
     dense = None
@@ -677,6 +732,12 @@ def run_lopa(args):
             line["cpu_baseline"] = cpu
         if cpu_all is not None:
             line["cpu_baseline_all_cores"] = cpu_all
+        if not args.no_cpu_baseline:
+            try:
+                line["decisions"] = oracle_step_report(full, tok, msk, nb, k, tau, st.out,
+                                                       bp_conf=None if bp is None else bp.conf)
+            except Exception as e:  # report, never hide the bench line
+                line["decisions"] = {"error": repr(e)}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()  # rank 0's CPU baseline runs while the others wait here

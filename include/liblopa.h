@@ -75,7 +75,9 @@ typedef enum {
 #define LOPA_DEV_NONFINITE 2  /* a reduced row holds NaN or +inf, or is all -inf (R20);
                                  that row's conf / argmax are unspecified                   */
 #define LOPA_DEV_PEER_TIMEOUT 4 /* lopa_bp_step_p2p: a peer's record did not arrive (bounded
-                                   wait); that step's decisions are unspecified            */
+                                   wait); that step decides nothing: n_branches_next = 0,
+                                   the next tables are left untouched.  Check dev_status
+                                   after every peer-memory step.                            */
 
 #define LOPA_MAX_WINDOW 256   /* W <= 256 (the D2F multi-block window); W > 64 needs V <= 2^22 */
 #define LOPA_MAX_BRANCHES 32  /* k + 1 <= 32: one lane per branch in the select             */
@@ -300,7 +302,9 @@ int lopa_syn_generate(uint64_t seed, int32_t block, int32_t vocab, int64_t ld, i
  *     communicator.
  *   lopa_bp_p2p_open: all_handles = the world handles in rank order (gathered by the caller);
  *     maps every peer's buffers.
- *   lopa_bp_step_p2p: as lopa_bp_step (args, b_loc), on the P2P buffers.
+ *   lopa_bp_step_p2p: as lopa_bp_step (args, b_loc), on the P2P buffers.  A peer that never
+ *     arrives within the bounded wait sets LOPA_DEV_PEER_TIMEOUT and ends the step with
+ *     n_branches_next = 0 (tables untouched): callers check dev_status after every step.
  * Errors: LOPA_ERR_INVALID_ARG (order of calls, sizes), LOPA_ERR_CUDA (allocation, IPC). */
 #define LOPA_BP_IPC_HANDLE_BYTES 64
 int lopa_bp_p2p_alloc(lopa_bp_t* bp, int32_t window, int32_t b_loc, size_t payload_bytes,

@@ -1752,6 +1752,19 @@ __global__ void bp_finish_kernel(const Params P, const uint8_t* records, int wor
       }
       if (v < epoch) atomicOr(P.dev_status, kDevPeerTimeout);
     }
+    // a rank that never arrived: decide nothing from stale or partial records -- the step ends
+    // with no branch (n_next = 0) and the tables untouched; the caller must check dev_status
+    // after every peer-memory step (liblopa.h, lopa_bp_step_p2p)
+    bool late = false;
+    if (lane < world) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + lane) : "memory");
+      late = v < epoch;
+    }
+    if (__any_sync(0xffffffffu, late)) {
+      if (lane == 0) *P.n_next = 0;
+      return;
+    }
     __syncwarp();
   }
   const size_t rb = record_bytes(b_loc);

@@ -507,13 +507,20 @@ static int launch_lmhead_chunk(const void* hidden, int64_t ld_hidden, const void
       !lmh::make_map(&mb256, weight, vocab, hidden_dim, ld_weight, 256) ||
       !lmh::make_map(&mb16, weight, vocab, hidden_dim, ld_weight, 16))
     return LOPA_ERR_CUDA;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(lmh::lopa_lmhead_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)lmh::kSmemBytes);
-  });
-  if (attr_err != cudaSuccess) return LOPA_ERR_CUDA;
+  // the kernel's shared-memory opt-in is per device context: set once per device
+  static std::mutex attr_mu;
+  static bool attr_done[64];
+  {
+    std::lock_guard<std::mutex> lk(attr_mu);
+    if (device < 0 || device >= 64) return LOPA_ERR_UNSUPPORTED;
+    if (!attr_done[device]) {
+      const cudaError_t e = cudaFuncSetAttribute(lmh::lopa_lmhead_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)lmh::kSmemBytes);
+      if (e != cudaSuccess) return cuda_status(e);
+      attr_done[device] = true;
+    }
+  }
   lmh::Args a;
   a.M = rows;
   a.K = hidden_dim;

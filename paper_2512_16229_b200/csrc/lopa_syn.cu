@@ -1,7 +1,7 @@
 // SYN-D2F synthetic logits on the device — the harness stand-in for the dLLM forward
 // (SURVEY.md §8(d)).  It implements the counter-based definition of
 // syngen/__init__.py independently (same integers, same bf16 bits) and holds none of LoPA's
-// arithmetic.  tests/test_gpu_syngen.py checks the two agree bit for bit.
+// arithmetic.  tests/test_gpu_parity.py::test_syn_generate_matches_numpy checks the two agree bit for bit.
 #include <cmath>
 #include <cstdint>
 

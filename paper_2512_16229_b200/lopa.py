@@ -426,8 +426,13 @@ class StepLoopGraph:
         for lg in logits:
             stepper._validate(lg, n_branches, branch_tokens, self.msk)
         self._args = [stepper.args(lg, n_branches, branch_tokens, self.msk) for lg in logits]
-        # warm up outside the capture (kernel attributes, lazy module loading)
+        # warm up outside the capture (kernel attributes, lazy module loading) on a snapshot of
+        # the caller's tables, restored afterwards: the first replay starts from the caller's state
+        snap = (self.tok.clone(), self.msk.clone(), self.nb.clone())
         self._iteration(0)
+        self.tok.copy_(snap[0])
+        self.msk.copy_(snap[1])
+        self.nb.copy_(snap[2])
         torch.cuda.synchronize(stepper.device)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):

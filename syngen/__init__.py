@@ -4,7 +4,7 @@ This module is the ONE piece shared by the oracle side (tests, `oracle/`) and th
 side (bench, GPU tests): it produces inputs only and holds none of LoPA's arithmetic
 (no softmax, no confidence, no Eq. 1 / Eq. 2, no top-k).  The CUDA kernel
 `lopa_syn_generate` (paper_2512_16229_b200/csrc/lopa_syn.cu) implements the same
-counter-based definition independently; `tests/test_gpu_syngen.py` checks the two
+counter-based definition independently; `tests/test_gpu_parity.py::test_syn_generate_matches_numpy` checks the two
 agree bit for bit.
 
 Definition ("SYN-D2F"; DESIGN.md §3 "Input recipe"):
