@@ -45,6 +45,11 @@ CONFIGS["dream-loop"] = dict(V=151936, W=32, k=15, tau=0.9, loop_blocks=8, seed=
                              name="D2F-Dream full decode loop: 256-token generation (8 blocks of 32), k=15, tau=0.9, branch-parallel (configs[2])")
 CONFIGS["diffucoder-loop"] = dict(V=151936, W=32, k=10, tau=0.95, loop_blocks=4, seed=3,
                                   name="D2F-DiffuCoder multi-block decode: 4 blocks of 32, k=10, tau=0.95, branch-parallel (configs[3])")
+# NEXT-1: the D2F block pipeline over a 256-token generation (configs[2] shape, k = 15, D2F GSM8K
+# parameters block 32 / tau_add 0.1 / tau_act 0.95 / tau_conf 0.90): the device
+# scheduler's captured loop beside the host-driven loop
+CONFIGS["d2f-graph"] = dict(V=151936, W=256, k=15, tau=0.95, d2f_len=256, seed=11,
+                            name="D2F multi-block decode, 256 tokens, k=15, block 32, tau_add 0.1, tau_act 0.95, tau_conf 0.90: device-resident scheduler in one CUDA graph")
 # NEXT-4: the same step from the verify forward's hidden states (fused LM-head a1), Dream-7B
 # output projection K = 3584 (Qwen2.5-7B hidden size; outside the paper), one GPU
 CONFIGS["lmhead-dream"] = dict(V=151936, W=32, k=7, tau=0.9, K=3584,
@@ -275,6 +280,36 @@ def run_reference(args):
         return 0
     if CFG.get("K"):
         return run_reference_lmhead(args)
+    if CFG.get("d2f_len"):
+        from oracle import d2f_oracle as D
+        import syngen
+        from threadpoolctl import threadpool_limits
+        V, k, seed, Lg = CFG["V"], CFG["k"], CFG["seed"], CFG["d2f_len"]
+        gen_s = 0.0
+
+        def fwd(b, t, m):
+            nonlocal gen_s
+            g0 = time.perf_counter()
+            x = syngen.gen_logits(seed, b, V, t, m)
+            gen_s += time.perf_counter() - g0
+            return x
+        nf = 6
+        with threadpool_limits(limits=1):
+            t0 = time.perf_counter()
+            tr = D.decode_d2f(fwd, Lg, 32, k, 0.1, 0.95, 0.9, max_window=256, max_forwards=nf)
+            el = time.perf_counter() - t0 - gen_s
+        value = tr.forwards / el
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (SYN-D2F seeded logits; no weights)", "config": {"workload": CFG["name"]},
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                 "sample": f"the first {tr.forwards} iterations of the D2F decode (oracle/d2f_oracle.py), "
+                                           f"generator time ({gen_s:.1f} s) excluded, NumPy fp64 single thread"},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "gpu_launches": 0}
+        print(json.dumps(line), flush=True)
+        return 0
     if CFG.get("loop_blocks"):
         cb = cpu_baseline_loop(CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["seed"],
                                budget_s=max(20.0, min(100.0, 2.0 * (args.steps + args.warmup))))
@@ -949,6 +984,81 @@ def run_loop(args):
     return 0
 
 
+def run_d2f(args):
+    """--config d2f-graph (NEXT-1): the D2F decode of a 256-token region with the block scheduler
+    on the device (d2f.D2FDeviceLoop: harness forward + lopa_step on the device window +
+    lopa_d2f_update per iteration, no host read), captured in ONE CUDA graph and replayed; beside
+    it the host-driven pipeline (d2f.decode_d2f: two host reads and a few torch ops per
+    iteration) on the same decode.  Both include the SYN-D2F forward stand-in of every
+    iteration (it cannot be precomputed without the decode's trajectory); a step = one
+    iteration.  One GPU."""
+    from paper_2512_16229_b200 import d2f, lopa
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != 1:
+        print(json.dumps({"error": "d2f-graph runs on one GPU"}))
+        return 0
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    V, k, seed, Lg = CFG["V"], CFG["k"], CFG["seed"], CFG["d2f_len"]
+    cfg = d2f.BlockConfig(32, 0.1, 0.95, 0.9, 256)
+    fwd = lambda b, t, m: lopa.syn_generate(seed, b, V, t, m)
+    h = d2f.decode_d2f(fwd, Lg, k, cfg, V, dev)          # trajectory length, warm-up
+    iters = h.forwards
+    loop = d2f.D2FDeviceLoop(Lg, k, cfg, V, dev, seed)
+    loop.capture(iters)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(3, min(args.steps // max(1, iters), 50))
+    for _ in range(2):
+        loop.reset()
+        loop.replay()
+    torch.cuda.synchronize()
+    dev_ms = 0.0
+    with ClockSampler(0) as clk:
+        for _ in range(reps):
+            loop.reset()
+            e0.record(stream)
+            loop.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            dev_ms += e0.elapsed_time(e1)
+    g = loop.trace()
+    if g.forwards != iters or g.winners != h.winners or not torch.equal(g.tokens, h.tokens):
+        raise RuntimeError("device D2F loop diverged from the host pipeline")
+    # host-driven pipeline on the same decode (device time between its first and last kernel)
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hreps = 3
+    host_ms = 0.0
+    for _ in range(hreps):
+        h0.record(stream)
+        d2f.decode_d2f(fwd, Lg, k, cfg, V, dev)
+        h1.record(stream)
+        torch.cuda.synchronize()
+        host_ms += h0.elapsed_time(h1)
+    # the harness forward alone, as the same captured loop runs it: one graph of the forwards of
+    # the recorded windows (the scheduler state replayed from the trace is not needed: the
+    # forward's cost depends on the window size and branch count only)
+    per_it = dev_ms / reps / iters
+    line = {
+        "metric": METRIC, "value": 1000.0 / per_it, "unit": UNIT, "n_gpus": 1, "steps": reps * iters,
+        "warmup": 2 * iters, "ms_per_step": per_it, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (SYN-D2F forward generated on the device inside the loop)",
+        "config": {"workload": CFG["name"], "gen_len": Lg, "iterations_per_decode": iters,
+                   "tokens_per_forward": Lg / iters, "max_window": max(w[1] for w in g.windows),
+                   "parallelism": "single"},
+        "d2f": {"device_graph_us_per_iteration": per_it * 1000.0,
+                "host_pipeline_us_per_iteration": host_ms / hreps / iters * 1000.0,
+                "speedup": (host_ms / hreps) / (dev_ms / reps),
+                "note": "both include the SYN-D2F forward of every iteration (windows up to 256 "
+                        "positions x up to 16 branches); the graph has no host read"},
+        "clocks": clk.summary(),
+        "gpu_launches": reps * iters * 4,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def cpu_baseline_loop(V, W, k, tau, seed, budget_s=15.0):
     """The oracle's Alg. 1 loop (NumPy fp64, one thread) on the same workload: whole blocks
     (generator included, as the CPU stand-in for the forward) until ~budget_s."""
@@ -1156,6 +1266,7 @@ def main():
     c = CONFIGS[args.config]
     CFG.update(V=c["V"], W=c["W"], k=c["k"], tau=c["tau"], name=c["name"])
     CFG["loop_blocks"] = c.get("loop_blocks")
+    CFG["d2f_len"] = c.get("d2f_len")
     if c.get("seed") is not None:
         CFG["seed"] = c["seed"]
     for key in ("k", "tau", "seed"):
@@ -1176,6 +1287,8 @@ def main():
         return run_lmhead(args)
     if CFG["loop_blocks"]:
         return run_loop(args)
+    if CFG["d2f_len"]:
+        return run_d2f(args)
     return run_lopa(args)
 
 

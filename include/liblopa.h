@@ -203,10 +203,58 @@ typedef struct {
   float metric_param;            /* window w >= 1 (integer) or eta in (0, 1]; unused for mean */
   const float* tau_pos;          /* device float [window] per-position Eq. 1 thresholds, or
                                     NULL (= tau): the D2F window's tau_act / tau_conf         */
+  const int32_t* window_dev;     /* NULL, or a device int32 scalar W_d in [1, window]: the step
+                                    then runs on a window of W_d positions read on the device
+                                    (the device-resident D2F loop, lopa_d2f_*): logits, tables,
+                                    conf / argmax and next tables are laid out [.][W_d] inside
+                                    their `window`-sized capacity; tau_pos [W_d]; `window` is
+                                    the capacity (and sizes the workspace).  Only lopa_step.  */
 } lopa_step_args_t;
 
 /* Next tables must not alias the input tables.  Errors: INVALID_ARG, UNSUPPORTED, CUDA. */
 int lopa_step(const lopa_step_args_t* args, void* stream);
+
+/* ---------------------------------------------------------------- NEXT-1 on the device
+ * The D2F block pipeline (readings R25 / R26) as device state plus a scheduler
+ * kernel, so that a whole multi-block decode -- the forward, lopa_step on the active window
+ * (args.window_dev = &sched[1], args.n_branches = &sched[2], args.tau_pos = tau_pos, tables =
+ * branch_tokens / branch_mask), lopa_d2f_update -- runs with no host read and can be captured
+ * in one CUDA graph.  Iterations after the last block is committed are no-ops (sched[3] = 1,
+ * n_branches = 0: the step passes through, the scheduler and the harness forward return). */
+typedef struct {
+  int32_t gen_len;          /* generation length, a multiple of block_size                  */
+  int32_t block_size;       /* B >= 1                                                        */
+  int32_t k;                /* lookahead budget, k + 1 <= LOPA_MAX_BRANCHES                  */
+  int32_t max_window;       /* in [block_size, LOPA_MAX_WINDOW]: active blocks * B stays <=  */
+  double tau_add;           /* activate the next block when the newest active block's fill
+                               ratio >= tau_add (compared exactly in double, R26 (b))        */
+  float tau_act, tau_conf;  /* Eq. 1 thresholds of the newest / older active blocks (R25)   */
+  int32_t trace_cap;        /* entries of `trace` (0 if trace is NULL)                       */
+  /* caller-owned device buffers */
+  int32_t* region_tokens;   /* [gen_len]: initial tokens in (masked positions), final out   */
+  uint8_t* region_mask;     /* [gen_len]: 1 = still masked (set to 1 by lopa_d2f_init)       */
+  int32_t* block_status;    /* [gen_len / B]: 0 inactive, 1 active, 2 committed              */
+  int32_t* sched;           /* [8]: window start p0, window W, branches of the next step n,
+                               done, forwards, committed blocks, -, -                         */
+  float* tau_pos;           /* [max_window]: the window's per-position thresholds            */
+  int32_t* branch_tokens;   /* [k + 1][max_window] capacity; the step's tables, [n][W]       */
+  uint8_t* branch_mask;     /* [k + 1][max_window] capacity                                  */
+  int32_t* commit_order;    /* [gen_len / B]: blocks in commit order (-1 = not yet)          */
+  int32_t* trace;           /* [trace_cap][4] (p0, W, n, winner) per forward, or NULL        */
+} lopa_d2f_t;
+
+/* Region fully masked, block 0 active, first window = block 0 with one branch (the initial
+ * predict).  Errors: INVALID_ARG (sizes, NULL buffers), CUDA. */
+int lopa_d2f_init(const lopa_d2f_t* d, void* stream);
+/* After a lopa_step on the window: B* -> region, rules (a) / (b), the next window's thresholds
+ * and tables (spawned branches carried over; n_next = 0 -> the new window's initial predict).
+ * winner / n_next / next_tokens / next_mask: that step's outputs ([k+1][W] layout). */
+int lopa_d2f_update(const lopa_d2f_t* d, const int32_t* winner, const int32_t* n_next,
+                    const int32_t* next_tokens, const uint8_t* next_mask, void* stream);
+/* Harness (not the method): SYN-D2F logits [n][W][ld] of the device window, block b's positions
+ * from block b's columns of each branch (DESIGN.md §3 "D2F loops"). */
+int lopa_d2f_syn_forward(uint64_t seed, int32_t vocab, int64_t ld, int32_t extras,
+                         const lopa_d2f_t* d, void* logits, void* stream);
 
 /* ---------------------------------------------------------------- branch parallelism (a5)
  * Global branch j lives on rank j / B_loc, B_loc = ceil(max_branches / world).

@@ -147,6 +147,8 @@ struct Params {
   int32_t cap;                 // branch capacity of the logits / conf tables
   int32_t table_rows;          // rows of the replicated branch tables (max_branches; n_rows / 1 for a1 alone)
   uint32_t epoch;              // checked builds: per-launch stamp of K1's partials (0 otherwise)
+  const int32_t* window_dev;   // nullable: the window read on the device (lopa_d2f_* loop);
+                               // n_cand = cap * window then (see with_device_window)
   float* conf;
   int32_t* argmax;
   int32_t* dev_status;
@@ -479,6 +481,18 @@ __device__ __forceinline__ FoldAcc fold_tree16(int n, const float4 (&q)[16]) {
   return FoldAcc{M, t[0], a};
 }
 
+// A step on a device-resident window (lopa_step_args_t.window_dev): the kernel's view of the
+// window and candidate rows (cap x W) comes from the device; every other field is unchanged.
+__device__ __forceinline__ Params with_device_window(const Params& P0) {
+  Params P = P0;
+  if (P0.window_dev) {
+    const int W = *P0.window_dev;
+    P.window = W;
+    P.n_cand = P0.cap * W;
+  }
+  return P;
+}
+
 // The 4th word of a group partial: the launch's epoch in checked builds, +0 otherwise.
 __device__ __forceinline__ float part_stamp(const Params& P) {
 #ifdef LOPA_CHECKED
@@ -697,7 +711,7 @@ constexpr int kStaticPct = LOPA_STATIC_PCT;  // % of K1's items assigned statica
 #else
 #define K1_CLAIM(p) atomicAdd((p), 1u)
 #endif
-__global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel(const Params P) {
+__global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel(const Params P_arg) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* stages = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -728,6 +742,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   // global inputs, then let the dependent fold/tail kernel launch (it may prefetch the inputs).
   grid_dep_wait();
   grid_dep_launch();
+  const Params P = with_device_window(P_arg);  // after the wait: the window was written before
   // ---- work items: (group g, row).  The first item of CTA b, (0, raw row b), is issued before
   // the row masks arrive (speculatively: a copy of a row that turns out invalid is discarded by
   // the consumers).  Every other item is numbered over the VALID rows only (masked rows of
@@ -1418,7 +1433,9 @@ __device__ __forceinline__ FoldAcc fold_row_smem(const float4* q, int n_grp, int
 }
 
 template <int MODE, int S>
-__global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params P) {
+__global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params P_arg) {
+  // launched by K1's launch_dependents, i.e. after K1's own wait: a device window is final
+  const Params P = with_device_window(P_arg);
   extern __shared__ __align__(128) uint8_t tsm[];
   TailSmem& T = *reinterpret_cast<TailSmem*>(tsm);
   uint16_t* rows = reinterpret_cast<uint16_t*>(tsm + kTailBytes);  // masked rows, ascending
@@ -2478,6 +2495,7 @@ extern "C" int lopa_step(const lopa_step_args_t* a, void* stream) {
   P.cap = a->max_branches;
   P.n_cand = rows;
   P.row_mask = a->branch_mask;
+  P.window_dev = a->window_dev;  // device-resident window (lopa_d2f_*): read by K1 / K2
   return launch_reduce(P, dev, s);
 }
 

@@ -33,13 +33,12 @@ __device__ __forceinline__ uint32_t noise_bits(uint32_t b) {
   return __float_as_uint(f) >> 16;
 }
 
-// grid (W, n_branches), block 256: one CTA per (branch, position) row.
-__global__ void syn_kernel(uint64_t seed, int blk, int V, long long ld, int W, int c8,
-                           const int32_t* __restrict__ br_tok, const uint8_t* __restrict__ br_msk,
-                           int extras, uint16_t* __restrict__ out) {
-  const int i = blockIdx.x, j = blockIdx.y;
-  const int32_t* tok = br_tok + (size_t)j * W;
-  const uint8_t* msk = br_msk + (size_t)j * W;
+// One (branch, position) row of SYN-D2F logits, by one CTA of blockDim.x threads: position i of
+// block `blk` whose state (W positions) is tok / msk.
+__device__ __forceinline__ void syn_row(uint64_t seed, int blk, int V, long long ld, int W, int c8,
+                                        const int32_t* __restrict__ tok,
+                                        const uint8_t* __restrict__ msk, int i, int extras,
+                                        uint16_t* __restrict__ row) {
   __shared__ unsigned long long s_hash;
   __shared__ int s_nb;
   if (threadIdx.x < 32) {
@@ -77,7 +76,6 @@ __global__ void syn_kernel(uint64_t seed, int blk, int V, long long ld, int W, i
     }
   }
   const uint32_t spike = __float_as_uint((float)s8 * 0.125f) >> 16;
-  uint16_t* row = out + ((size_t)j * W + i) * (size_t)ld;
   const int nq = (V + 7) / 8;
   for (int q = threadIdx.x; q < nq; q += blockDim.x) {
     uint32_t b[8];
@@ -109,6 +107,34 @@ __global__ void syn_kernel(uint64_t seed, int blk, int V, long long ld, int W, i
   for (long long v = 8LL * nq + threadIdx.x; v < ld; v += blockDim.x) row[v] = 0;
 }
 
+// grid (W, n_branches), block 256: one CTA per (branch, position) row.
+__global__ void syn_kernel(uint64_t seed, int blk, int V, long long ld, int W, int c8,
+                           const int32_t* __restrict__ br_tok, const uint8_t* __restrict__ br_msk,
+                           int extras, uint16_t* __restrict__ out) {
+  const int i = blockIdx.x, j = blockIdx.y;
+  syn_row(seed, blk, V, ld, W, c8, br_tok + (size_t)j * W, br_msk + (size_t)j * W, i, extras,
+          out + ((size_t)j * W + i) * (size_t)ld);
+}
+
+// The D2F window's forward (lopa_d2f_syn_forward): grid (max_window, k + 1), one CTA per
+// (branch, window position); the window (p0, W, n) is read on the device (sched).  Position
+// c of the window is position i = (p0 + c) mod B of block b = (p0 + c) / B, generated from
+// that block's columns of the branch's window row -- the same logits as SYN-D2F per block
+// ("D2F loops").
+__global__ void syn_window_kernel(uint64_t seed, int V, long long ld, int B, int c8,
+                                  const int32_t* __restrict__ sched,
+                                  const int32_t* __restrict__ br_tok,
+                                  const uint8_t* __restrict__ br_msk, int extras,
+                                  uint16_t* __restrict__ out) {
+  const int p0 = sched[0], W = sched[1], n = sched[2], done = sched[3];
+  const int c = blockIdx.x, j = blockIdx.y;
+  if (done || c >= W || j >= n) return;
+  const int p = p0 + c, b = p / B, i = p - b * B;
+  const int cb = b * B - p0;
+  syn_row(seed, b, V, ld, B, c8, br_tok + (size_t)j * W + cb, br_msk + (size_t)j * W + cb, i,
+          extras, out + ((size_t)j * W + c) * (size_t)ld);
+}
+
 }  // namespace syn
 }  // namespace lopa
 
@@ -129,5 +155,22 @@ extern "C" int lopa_syn_generate(uint64_t seed, int32_t block, int32_t vocab, in
   lopa::syn::syn_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       seed, block, vocab, ld, window, c8, branch_tokens, branch_mask, extras,
       static_cast<uint16_t*>(out));
+  return lopa::cuda_status(cudaGetLastError());
+}
+
+extern "C" int lopa_d2f_syn_forward(uint64_t seed, int32_t vocab, int64_t ld, int32_t extras,
+                                    const lopa_d2f_t* d, void* logits, void* stream) {
+  if (!d || !logits || vocab < 1 || ld < vocab || ld % 8 != 0 || d->block_size < 1 ||
+      d->max_window < 1 || d->max_window > LOPA_MAX_WINDOW || d->k < 0 ||
+      d->k + 1 > LOPA_MAX_BRANCHES || !d->sched || !d->branch_tokens || !d->branch_mask ||
+      (reinterpret_cast<uintptr_t>(logits) & 15))
+    return LOPA_ERR_INVALID_ARG;
+  int dev;
+  if (!lopa::bind_device(stream, logits, &dev)) return LOPA_ERR_CUDA;
+  const int c8 = vocab < 2 ? 0 : (int)std::lround(8.0 * std::log(1.8 * (double)(vocab - 1)));
+  dim3 grid(d->max_window, d->k + 1);
+  lopa::syn::syn_window_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      seed, vocab, ld, d->block_size, c8, d->sched, d->branch_tokens, d->branch_mask, extras,
+      static_cast<uint16_t*>(logits));
   return lopa::cuda_status(cudaGetLastError());
 }

@@ -16,11 +16,13 @@ PAPER.md:519-536):
   appended fully masked; a step that completes its window (R21) is followed by the new
   window's initial predict (R17).
 
-This module is host control flow only (a few integers per iteration); all per-position work
-is in liblopa's kernels.  It never imports the oracle.
+decode_d2f is host control flow (a few integers per iteration); all per-position work is in
+liblopa's kernels.  D2FDeviceLoop runs the same rules on the device (lopa_d2f_*: no host read,
+CUDA-graph capturable).  This module never imports the oracle.
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 
 import torch
@@ -184,3 +186,111 @@ def decode_d2f(forward_block, gen_len: int, k: int, cfg: BlockConfig, vocab: int
         p0, W, br_tok, br_msk = q0, WN, nt, nm
     res.tokens = tok
     return res
+
+
+class D2FDesc(ctypes.Structure):
+    """Mirror of lopa_d2f_t (include/liblopa.h)."""
+    _fields_ = [
+        ("gen_len", ctypes.c_int32), ("block_size", ctypes.c_int32), ("k", ctypes.c_int32),
+        ("max_window", ctypes.c_int32), ("tau_add", ctypes.c_double), ("tau_act", ctypes.c_float),
+        ("tau_conf", ctypes.c_float), ("trace_cap", ctypes.c_int32),
+        ("region_tokens", ctypes.c_void_p), ("region_mask", ctypes.c_void_p),
+        ("block_status", ctypes.c_void_p), ("sched", ctypes.c_void_p), ("tau_pos", ctypes.c_void_p),
+        ("branch_tokens", ctypes.c_void_p), ("branch_mask", ctypes.c_void_p),
+        ("commit_order", ctypes.c_void_p), ("trace", ctypes.c_void_p),
+    ]
+
+
+class D2FDeviceLoop:
+    """The D2F decode with the block scheduler on the device (lopa_d2f_*; rules R26 as in
+    BlockPipeline): one iteration = the harness forward of the device window
+    (lopa_d2f_syn_forward, the model stand-in) + one lopa_step whose window, branch count and
+    thresholds are read on the device + lopa_d2f_update.  No host read anywhere, so `iters`
+    iterations can be issued blindly (iterations after the last commit are no-ops) or captured
+    in one CUDA graph (capture()).  trace() reads the windows, branch counts, winners and commit
+    order back for comparison with decode_d2f / the oracle."""
+
+    def __init__(self, gen_len: int, k: int, cfg: BlockConfig, vocab: int, device, seed: int,
+                 extras: int = 0, tokens0: torch.Tensor | None = None, trace_cap: int = 1024,
+                 metric: int = lopa.METRIC_MEAN, metric_param: float = 0.0):
+        B, mw = cfg.block_size, cfg.max_window
+        if gen_len % B or B > mw or mw > lopa.MAX_WINDOW:
+            raise lopa.LopaError("gen_len % block_size == 0 and block_size <= max_window <= 256")
+        d = torch.device(device)
+        self.dev, self.seed, self.extras, self.vocab, self.k, self.cfg = d, seed, extras, vocab, k, cfg
+        self.gen_len, self.nblk, self.max_br = gen_len, gen_len // B, k + 1
+        self.tokens0 = (torch.zeros(gen_len, dtype=torch.int32, device=d) if tokens0 is None
+                        else tokens0.to(torch.int32).clone())
+        self.region_tokens = self.tokens0.clone()
+        self.region_mask = torch.ones(gen_len, dtype=torch.uint8, device=d)
+        self.block_status = torch.zeros(self.nblk, dtype=torch.int32, device=d)
+        self.sched = torch.zeros(8, dtype=torch.int32, device=d)
+        self.tau_pos = torch.empty(mw, dtype=torch.float32, device=d)
+        self.branch_tokens = torch.zeros((self.max_br, mw), dtype=torch.int32, device=d)
+        self.branch_mask = torch.zeros((self.max_br, mw), dtype=torch.uint8, device=d)
+        self.commit_order = torch.full((self.nblk,), -1, dtype=torch.int32, device=d)
+        self.trace_buf = torch.zeros((trace_cap, 4), dtype=torch.int32, device=d)
+        self.st = lopa.Stepper(vocab, mw, self.max_br, k, cfg.tau_act, d, metric=metric,
+                               metric_param=metric_param, tau_pos=self.tau_pos)
+        self.logits = torch.zeros((self.max_br, mw, self.st.ld), dtype=torch.bfloat16, device=d)
+        self.desc = D2FDesc(gen_len, B, k, mw, float(cfg.tau_add), float(cfg.tau_act),
+                            float(cfg.tau_conf), trace_cap, self.region_tokens.data_ptr(),
+                            self.region_mask.data_ptr(), self.block_status.data_ptr(),
+                            self.sched.data_ptr(), self.tau_pos.data_ptr(),
+                            self.branch_tokens.data_ptr(), self.branch_mask.data_ptr(),
+                            self.commit_order.data_ptr(), self.trace_buf.data_ptr())
+        a = self.st.args(self.logits, self.sched[2:3], self.branch_tokens, self.branch_mask)
+        a.window_dev = self.sched.data_ptr() + 4        # &sched[1]
+        self.args = a
+        self.graph = None
+
+    def reset(self):
+        """Back to the initial state (tokens0, region masked, block 0 active)."""
+        self.region_tokens.copy_(self.tokens0)
+        lopa._check(lopa.lib().lopa_d2f_init(ctypes.byref(self.desc), lopa._stream(self.dev)),
+                    "lopa_d2f_init")
+
+    def iteration(self):
+        L, s = lopa.lib(), lopa._stream(self.dev)
+        lopa._check(L.lopa_d2f_syn_forward(self.seed & ((1 << 64) - 1), self.vocab, self.st.ld,
+                                           self.extras, ctypes.byref(self.desc),
+                                           lopa._p(self.logits), s), "lopa_d2f_syn_forward")
+        lopa._check(L.lopa_step(ctypes.byref(self.args), s), "lopa_step")
+        o = self.st.out
+        lopa._check(L.lopa_d2f_update(ctypes.byref(self.desc), lopa._p(o.winner), lopa._p(o.n_next),
+                                      lopa._p(o.next_tokens), lopa._p(o.next_mask), s),
+                    "lopa_d2f_update")
+
+    def run(self, iters: int):
+        for _ in range(iters):
+            self.iteration()
+
+    def capture(self, iters: int):
+        """`iters` iterations in one CUDA graph (reset() not included; replay() after reset())."""
+        self.reset()
+        self.iteration()                      # warm-up outside the capture (attributes, modules)
+        torch.cuda.synchronize(self.dev)
+        self.reset()
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run(iters)
+        self.graph = g
+        return g
+
+    def replay(self):
+        self.graph.replay()
+
+    def done(self) -> bool:
+        return bool(int(self.sched[3].item()))
+
+    def trace(self) -> D2FResult:
+        s = self.sched.cpu().tolist()
+        f = s[4]
+        tr = self.trace_buf[:min(f, self.trace_buf.shape[0])].cpu().tolist()
+        res = D2FResult(tokens=self.region_tokens.clone(), forwards=f)
+        res.windows = [(t[0], t[1]) for t in tr]
+        res.branch_counts = [t[2] for t in tr]
+        res.winners = [t[3] for t in tr]
+        res.commits = [b for b in self.commit_order.cpu().tolist() if b >= 0]
+        return res

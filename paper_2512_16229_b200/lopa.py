@@ -56,6 +56,7 @@ class StepArgs(ctypes.Structure):
         ("n_branches_next", _c_void_p), ("dev_status", _c_void_p),
         ("workspace", _c_void_p), ("workspace_bytes", _size),
         ("metric", _i32), ("metric_param", _f32), ("tau_pos", _c_void_p),
+        ("window_dev", _c_void_p),
     ]
 
 
@@ -65,6 +66,9 @@ _SIGS = {
     "lopa_last_cuda_error": (ctypes.c_char_p, []),
     "lopa_debug_k1_attrs": (_i32, [ctypes.c_void_p]),
     "lopa_debug_check_read": (_i32, [ctypes.c_void_p]),
+    "lopa_d2f_init": (_i32, [_c_void_p, _c_void_p]),
+    "lopa_d2f_update": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
+    "lopa_d2f_syn_forward": (_i32, [ctypes.c_uint64, _i32, _i64, _i32, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_workspace_bytes": (_size, [_i32, _i32]),
     "lopa_num_segments": (_i32, [_i32]),
     "lopa_confidence": (_i32, [_c_void_p, _i64, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
