@@ -79,6 +79,9 @@ typedef enum {
                                    the next tables are left untouched.  Check dev_status
                                    after every peer-memory step.                            */
 
+#define LOPA_DEV_INTERNAL 8   /* internal protocol error: a partial of the reduction never
+                                 arrived within the fold's bounded poll (a fault upstream)  */
+
 #define LOPA_MAX_WINDOW 256   /* W <= 256 (the D2F multi-block window); W > 64 needs V <= 2^22 */
 #define LOPA_MAX_BRANCHES 32  /* k + 1 <= 32: one lane per branch in the select             */
 #define LOPA_MAX_ROWS 4096    /* rows per call: n_rows, or max_branches * window            */
@@ -327,6 +330,8 @@ int lopa_debug_ldg_timeline(unsigned long long* out, int n_words);
 /* Debug: per-item timeline of the TMA-form K1's last launch (-DLOPA_K1_TL builds only); same
  * return convention. */
 int lopa_debug_k1_timeline(unsigned long long* out, int n_words);
+/* Debug: per-step marks of chained steps (-DLOPA_CHAIN_TL builds only), [64][8] ns; cleared. */
+int lopa_debug_chain_timeline(unsigned long long* out, int n_words);
 
 /* ---------------------------------------------------------------- harness (not the method)
  * SYN-D2F synthetic logits for a batch of branch states (the stand-in for the dLLM forward;

@@ -146,7 +146,7 @@ struct Params {
   int32_t branch_base;         // global id of logits branch 0 (BP local)
   int32_t cap;                 // branch capacity of the logits / conf tables
   int32_t table_rows;          // rows of the replicated branch tables (max_branches; n_rows / 1 for a1 alone)
-  uint32_t epoch;              // checked builds: per-launch stamp of K1's partials (0 otherwise)
+  int32_t k1_alone;            // K1 launched without a consumer (lopa_debug_reduce_only)
   const int32_t* window_dev;   // nullable: the window read on the device (lopa_d2f_* loop);
                                // n_cand = cap * window then (see with_device_window)
   float* conf;
@@ -493,15 +493,47 @@ __device__ __forceinline__ Params with_device_window(const Params& P0) {
   return P;
 }
 
-// The 4th word of a group partial: the launch's epoch in checked builds, +0 otherwise.
-__device__ __forceinline__ float part_stamp(const Params& P) {
-#ifdef LOPA_CHECKED
-  return __uint_as_float(P.epoch);
-#else
-  (void)P;
-  return 0.f;
-#endif
+// ------------------------------------------------------------------ group partials
+// A group partial (the fold of one (group, row) work item) occupies one 16-byte workspace slot
+// as TWO 64-bit words, each single-copy atomic and each stamped with the launch's epoch
+// (workspace counter ctrs[2] + 1), so that a reader can tell a partial of THIS launch from a
+// stale one without any fence on the writer's side:
+//   A = S bits | (M's bf16 bits << 32) | (stamp & 0xFFFF) << 48    (M is a max of bf16 logits:
+//       its low 16 bits are zero, so the bf16 bits are lossless)
+//   B = argmax | stamp << 32
+// K2 therefore folds each row as soon as its partials have landed, while K1 still streams, and
+// waits for K1's grid only at its very end (LOPA_NO_K2_POLL: the round-1 hand-off, K2 waits for
+// K1's grid before reading the partials).  Epoch protocol: K1 reads e = ctrs[2] after its grid
+// dependency wait and stamps e + 1; the launch's consumer (K2, the fold kernel, or K1 itself
+// when launched alone) stores ctrs[2] = e + 1 once K1 has completed, so every K1 launch stamps
+// a fresh epoch, also across CUDA-graph replays.
+__device__ __forceinline__ void store_partial(float4* slot, const FoldAcc& f, uint32_t stamp) {
+  const uint64_t A = (uint64_t)__float_as_uint(f.S) | ((uint64_t)(__float_as_uint(f.M) >> 16) << 32) |
+                     ((uint64_t)(stamp & 0xFFFFu) << 48);
+  const uint64_t B = (uint64_t)f.a | ((uint64_t)stamp << 32);
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(slot), "l"(A), "l"(B) : "memory");
 }
+__device__ __forceinline__ float4 decode_partial(uint64_t A, uint64_t B) {
+  return make_float4(__uint_as_float(((uint32_t)(A >> 32) & 0xFFFFu) << 16), __uint_as_float((uint32_t)A),
+                     __uint_as_float((uint32_t)B), 0.f);
+}
+__device__ __forceinline__ bool stamped(uint64_t A, uint64_t B, uint32_t stamp) {
+  return (uint32_t)(B >> 32) == stamp && (uint32_t)(A >> 48) == (stamp & 0xFFFFu);
+}
+__device__ __forceinline__ void load_stamp_half(const float4* slot, uint64_t* B) {
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(*B) : "l"(reinterpret_cast<const char*>(slot) + 8) : "memory");
+}
+__device__ __forceinline__ void load_partial_raw(const float4* slot, uint64_t* A, uint64_t* B) {
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(*A), "=l"(*B) : "l"(slot) : "memory");
+}
+// A slot staged in shared memory (bulk copy after K1 completed) -> (M, S, argmax bits, -).
+__device__ __forceinline__ float4 decode_slot(const float4& q, uint32_t* stamp) {
+  const uint64_t A = (uint64_t)__float_as_uint(q.x) | ((uint64_t)__float_as_uint(q.y) << 32);
+  const uint64_t B = (uint64_t)__float_as_uint(q.z) | ((uint64_t)__float_as_uint(q.w) << 32);
+  *stamp = (uint32_t)(B >> 32);
+  return decode_partial(A, B);
+}
+constexpr uint32_t kPollSpins = 1u << 22;  // ~0.5 s at 100 ns: a K1 that never arrives is an error
 
 // ------------------------------------------------------------------ K2's decision tail
 // Everything the decision tail needs, staged in K2's shared memory.
@@ -699,6 +731,24 @@ __device__ __forceinline__ unsigned long long k1_gtime() {
 #else
 #define K1TL(idx) ((void)0)
 #endif
+#ifdef LOPA_CHAIN_TL
+// experiment: per-step %globaltimer marks of chained steps, indexed by the partial epoch:
+// [epoch % 64][0 K1 first CTA start, 1 K1 last CTA end, 2 K2 start, 3 K2 rows folded,
+//  4 K2 decisions done, 5 K2 final wait returned, 6 K1 first CTA after its wait]
+__device__ unsigned long long g_chain[64][8];
+__device__ __forceinline__ unsigned long long ch_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CHMIN(e, s) atomicMin(&g_chain[(e) & 63][(s)], ch_now())
+#define CHMAX(e, s) atomicMax(&g_chain[(e) & 63][(s)], ch_now())
+#define CHSET(e, s) (g_chain[(e) & 63][(s)] = ch_now())
+#else
+#define CHMIN(e, s) ((void)0)
+#define CHMAX(e, s) ((void)0)
+#define CHSET(e, s) ((void)0)
+#endif
 // A work claim.  LOPA_TMA_ASM_ATOM: one atom instruction whose value is waited for where it is
 // used (atomicAdd is warp-aggregated by the compiler: vote + shuffle of the returned value,
 // which waits for the round trip at the call).
@@ -743,6 +793,8 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   grid_dep_wait();
   grid_dep_launch();
   const Params P = with_device_window(P_arg);  // after the wait: the window was written before
+  const uint32_t stamp = P.ctrs[2] + 1u;          // this launch's partial epoch
+  if (tid == 0) CHMIN(stamp, 6);
   // ---- work items: (group g, row).  The first item of CTA b, (0, raw row b), is issued before
   // the row masks arrive (speculatively: a copy of a row that turns out invalid is discarded by
   // the consumers).  Every other item is numbered over the VALID rows only (masked rows of
@@ -916,6 +968,9 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
         __threadfence();
         P.ctrs[0] = 0;
         P.ctrs[1] = 0;
+        // no polling consumer (K1 alone, or the fold kernel, which waits for K1's grid): K1
+        // advances the epoch itself
+        if (P.k1_alone || P.mode == MODE_CONF) P.ctrs[2] = stamp;
       }
       // end-of-work sentinels: one stage per consumer phase (every warpgroup sees one)
       for (int c = 0; c < kWgStride; ++c, ++i) {
@@ -978,7 +1033,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
           const float4* q = ipart + slot * kPartPerItem;
           const FoldAcc f = fold_seq(kWarpsPerSeg * nsi, [&](int p) { return q[p]; });
           LOPA_CHK(g >= 0 && g < P.n_grp && row >= 0 && row < P.n_cand, 3);
-          P.gpart[(size_t)g * P.n_cand + row] = make_float4(f.M, f.S, __uint_as_float(f.a), part_stamp(P));
+          store_partial(P.gpart + (size_t)g * P.n_cand + row, f, stamp);
           icnt[slot] = 0;
           mbar_arrive(&slot_free[slot]);
         }
@@ -988,6 +1043,8 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   }
 
   if (tid == 0) TL(4);
+  __syncthreads();
+  if (tid == 0) CHMAX(stamp, 1);
 }
 
 // ------------------------------------------------------------------ K1, warp-staged form
@@ -1345,7 +1402,7 @@ __global__ void __launch_bounds__(kLThreads, 1) lopa_reduce_ldg_kernel(const Par
         if (valid) {
           const float4* qp = ipart[team][t.slot];
           const FoldAcc f = fold_seq(kWarpsPerSeg * t.nsi, [&](int p) { return qp[p]; });
-          P.gpart[(size_t)t.g * P.n_cand + t.row] = make_float4(f.M, f.S, __uint_as_float(f.a), 0.f);
+          store_partial(P.gpart + (size_t)t.g * P.n_cand + t.row, f, P.ctrs[2] + 1u);
         }
         icnt[team][t.slot] = 0;
         mbar_arrive(&sfree[team][t.slot]);
@@ -1397,13 +1454,24 @@ __global__ void __launch_bounds__(kLThreads, 1) lopa_reduce_ldg_kernel(const Par
 // griddepcontrol.wait returns once K1's writes are visible.  It folds every masked row's group
 // partials in fixed order (conf bits depend only on the row's bytes) and runs the tail.
 #ifndef LOPA_TAIL_THREADS
+#ifdef LOPA_NO_K2_POLL
 #define LOPA_TAIL_THREADS 512
+#else
+// the polling fold keeps 16 slots' loads in flight per thread: 256 threads leave it 255
+// registers (512 threads cap it at 128 and spill; measured 21.96 vs 20.37 us per Dream step)
+#define LOPA_TAIL_THREADS 256
+#endif
 #endif
 constexpr int kTailThreads = LOPA_TAIL_THREADS;
 // K1's group partials are pulled into K2's shared memory with ONE bulk copy when they fit
 // (the Dream step: 10 groups x 256 rows x 16 B = 41 KB): a single L2 round trip instead of
 // ten loads per thread.
+#ifdef LOPA_NO_K2_POLL
 constexpr size_t kGpStageBytes = 64 * 1024;
+#else
+// polling fold: each thread's 16 decoded partials in a private scratch column ([16][threads])
+constexpr size_t kGpStageBytes = (size_t)16 * LOPA_TAIL_THREADS * 16;
+#endif
 constexpr size_t kTailSmemBytes = kTailBytes + LOPA_MAX_ROWS * 2 + 16 + kGpStageBytes;
 
 
@@ -1441,6 +1509,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   uint16_t* rows = reinterpret_cast<uint16_t*>(tsm + kTailBytes);  // masked rows, ascending
   uint64_t* gbar = reinterpret_cast<uint64_t*>(tsm + kTailBytes + LOPA_MAX_ROWS * 2);
   float4* gst = reinterpret_cast<float4*>(tsm + kTailBytes + LOPA_MAX_ROWS * 2 + 16);
+  float4* pscr = gst;  // polling fold's per-thread scratch (the staged copy is unused then)
   const size_t gbytes = (size_t)P.n_grp * P.n_cand * sizeof(float4);
   const bool staged = MODE != MODE_DECIDE && gbytes <= kGpStageBytes;
   if (threadIdx.x == 0 && staged) {
@@ -1450,7 +1519,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   // When 16 group slots of every row fit, the slots past n_grp hold neutral partials
   // (m = -inf, s = 0), so the 16-slot fold runs without predicates (identical bits: a neutral
   // slot adds +0 and never matches the maximum).
+#ifdef LOPA_NO_K2_POLL
   const bool staged16 = staged && P.n_grp <= 16 && (size_t)P.n_cand * 16 * sizeof(float4) <= kGpStageBytes;
+#else
+  const bool staged16 = false;  // the polling fold decodes into per-thread scratch instead
+#endif
   if (staged16) {
     const float4 neutral = make_float4(-INFINITY, 0.f, __uint_as_float(0xFFFFFFFFu), 0.f);
     for (int e = threadIdx.x; e < (16 - P.n_grp) * P.n_cand; e += kTailThreads)
@@ -1533,9 +1606,95 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   }
 #endif
   __syncthreads();
+  const int n_grp = P.n_grp;
+  const uint32_t stamp = P.ctrs[2] + 1u;  // the epoch K1 stamps (ctrs[2] is constant during K1)
+  if (tid == 0) CHSET(stamp, 2);
+#ifndef LOPA_NO_K2_POLL
+  if (MODE != MODE_DECIDE) {
+    // Fold every masked row as soon as its n_grp partials of THIS launch have landed (each
+    // 64-bit half self-validating, store_partial), while K1 still streams: no grid-wide wait.
+    for (int rc = tid; rc < n_masked; rc += kTailThreads) {
+      const int row = rows[rc];
+      const float4* q = P.gpart + row;
+      FoldAcc f;
+      if (n_grp <= 16) {
+        // poll the row's pending slots (all loads in flight at once); a slot whose two halves
+        // both carry this launch's epoch is decoded into this thread's scratch column
+        uint32_t pend = (1u << n_grp) - 1u;
+        for (uint32_t spin = 0;; ++spin) {
+#pragma unroll
+          for (int h = 0; h < 16; h += 8) {  // two batches of 8 loads in flight
+            uint64_t A[8], B[8];
+#pragma unroll
+            for (int p = 0; p < 8; ++p)
+              if ((pend >> (h + p)) & 1u) load_partial_raw(q + (size_t)(h + p) * P.n_cand, &A[p], &B[p]);
+#pragma unroll
+            for (int p = 0; p < 8; ++p)
+              if (((pend >> (h + p)) & 1u) && stamped(A[p], B[p], stamp)) {
+                pscr[(h + p) * kTailThreads + tid] = decode_partial(A[p], B[p]);
+                pend &= ~(1u << (h + p));
+              }
+          }
+          if (!pend) break;
+          if (spin >= kPollSpins) {
+            atomicOr(P.dev_status, kDevInternal);
+            LOPA_CHK(false, 6);
+            break;
+          }
+          __nanosleep(64);
+        }
+        float4 qr[16];
+#pragma unroll
+        for (int p = 0; p < 16; ++p)
+          qr[p] = (p < n_grp && !((pend >> p) & 1u))
+                      ? pscr[p * kTailThreads + tid]
+                      : make_float4(-INFINITY, 0.f, __uint_as_float(0xFFFFFFFFu), 0.f);
+        f = fold_tree16(n_grp, qr);
+      } else {
+        // > 16 groups (V > 2^18): poll each partial in turn, then the sequential fold re-reads
+        // them (already stamped, so the values are final)
+        for (int p = 0; p < n_grp; ++p) {
+          uint64_t A, B;
+          uint32_t spin = 0;
+          for (load_partial_raw(q + (size_t)p * P.n_cand, &A, &B); !stamped(A, B, stamp);
+               load_partial_raw(q + (size_t)p * P.n_cand, &A, &B)) {
+            if (++spin >= kPollSpins) {
+              atomicOr(P.dev_status, kDevInternal);
+              LOPA_CHK(false, 6);
+              break;
+            }
+            __nanosleep(64);
+          }
+        }
+        f = fold_seq(n_grp, [&](int p) {
+          uint64_t A, B;
+          load_partial_raw(q + (size_t)p * P.n_cand, &A, &B);
+          return decode_partial(A, B);
+        });
+      }
+      LOPA_CHK(row < P.n_cand, 7);
+#ifdef LOPA_TIMELINE
+      if (rc == 0) tl_clk_dep(17, f.S);
+#endif
+      const float c = __fdiv_rn(1.0f, f.S);
+      P.conf[row] = c;
+      P.argmax[row] = (int32_t)f.a;
+      if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
+      T.conf[row] = c;
+      T.amax[row] = (int32_t)f.a;
+    }
+  } else {
+    grid_dep_wait();  // MODE_DECIDE: conf / argmax written by the previous kernel
+    for (int rc = tid; rc < n_masked; rc += kTailThreads) {
+      const int row = rows[rc];
+      T.conf[row] = __ldcg(P.conf + row);
+      T.amax[row] = __ldcg(P.argmax + row);
+    }
+  }
+  if (tid == 0) { TL(6); TLC(16); }
+#else
   grid_dep_wait();  // K1's group partials are visible from here on
   if (tid == 0) { TL(6); TLC(16); }
-  const int n_grp = P.n_grp;
   if (MODE == MODE_DECIDE) {
     for (int rc = tid; rc < n_masked; rc += kTailThreads) {
       const int row = rows[rc];
@@ -1548,48 +1707,25 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
       bulk_g2s(gst, P.gpart, (uint32_t)gbytes, gbar, policy_evict_first());
     }
     mbar_wait(gbar, 0);
-    if (tid == 0) TLC(23);
     const int stride = P.n_cand;
     for (int rc = tid; rc < n_masked; rc += kTailThreads) {
       const int row = rows[rc];
-      if (staged16) {
-        float4 qr[16];
-#pragma unroll
-        for (int p = 0; p < 16; ++p) qr[p] = gst[row + p * stride];
-#ifdef LOPA_CHECKED
-        for (int p = 0; p < n_grp; ++p) LOPA_CHK(__float_as_uint(qr[p].w) == P.epoch, 6);
-        LOPA_CHK(row < P.n_cand, 7);
-#endif
-        const FoldAcc f = fold_tree16(16, qr);
-#ifdef LOPA_TIMELINE
-        if (rc == 0) tl_clk_dep(17, f.S);
-#endif
-        const float c = __fdiv_rn(1.0f, f.S);
-        P.conf[row] = c;
-        P.argmax[row] = (int32_t)f.a;
-        if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
-        T.conf[row] = c;
-        T.amax[row] = (int32_t)f.a;
-        continue;
+      float4 qr[16];
+      uint32_t st_bad = 0;
+      for (int p = 0; p < 16; ++p) {
+        uint32_t sp = stamp;
+        qr[p] = p < n_grp ? decode_slot(gst[row + p * stride], &sp)
+                          : make_float4(-INFINITY, 0.f, __uint_as_float(0xFFFFFFFFu), 0.f);
+        st_bad |= sp != stamp;
       }
-#ifdef LOPA_TIMELINE
-      if (rc == 0) {
-        const float4 q0 = gst[row];
-        tl_clk_dep(21, q0.x);  // one staged partial read back
-      }
-#endif
-#ifdef LOPA_CHECKED
-      for (int p = 0; p < n_grp; ++p) LOPA_CHK(__float_as_uint(gst[row + p * P.n_cand].w) == P.epoch, 6);
+      LOPA_CHK(!st_bad, 6);
       LOPA_CHK(row < P.n_cand, 7);
-#endif
-      const FoldAcc f = fold_row_smem(gst + row, n_grp, P.n_cand);
-#ifdef LOPA_TIMELINE
-      if (rc == 0) tl_clk_dep(17, f.S);
-#endif
+      const FoldAcc f = n_grp <= 16 ? fold_tree16(n_grp, qr)
+                                    : fold_seq(n_grp, [&](int p) {
+                                        uint32_t sp;
+                                        return decode_slot(gst[row + p * stride], &sp);
+                                      });
       const float c = __fdiv_rn(1.0f, f.S);
-#ifdef LOPA_TIMELINE
-      if (rc == 0) tl_clk_dep(22, c);
-#endif
       P.conf[row] = c;
       P.argmax[row] = (int32_t)f.a;
       if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
@@ -1599,12 +1735,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   } else
   for (int rc = tid; rc < n_masked; rc += kTailThreads) {
     const int row = rows[rc];
-#ifdef LOPA_CHECKED
-    for (int p = 0; p < n_grp; ++p)
-      LOPA_CHK(__float_as_uint(__ldcg(P.gpart + row + (size_t)p * P.n_cand).w) == P.epoch, 6);
-    LOPA_CHK(row < P.n_cand, 7);
-#endif
-    const FoldAcc f = fold_row_global(P.gpart + row, n_grp, (size_t)P.n_cand);
+    const FoldAcc f = fold_seq(n_grp, [&](int p) {
+      uint64_t A, B;
+      load_partial_raw(P.gpart + row + (size_t)p * P.n_cand, &A, &B);
+      return decode_partial(A, B);
+    });
     const float c = __fdiv_rn(1.0f, f.S);
     P.conf[row] = c;
     P.argmax[row] = (int32_t)f.a;
@@ -1612,14 +1747,23 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
     T.conf[row] = c;
     T.amax[row] = (int32_t)f.a;
   }
+#endif
   if (tid == 0) TLC(18);
   __syncthreads();
-  if (tid == 0) { TL(7); TLC(19); }
+  if (tid == 0) { TL(7); TLC(19); CHSET(stamp, 3); }
   if (MODE == MODE_STEP || MODE == MODE_DECIDE) cta_tail_step<kTailThreads, S>(P, T, tid, nb);
   if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads, S>(P, T, tid, nb);
   if (tid == 0) {
     TL(5);
     TLC(20);
+  }
+  if (tid == 0) CHSET(stamp, 4);
+  if (MODE != MODE_DECIDE) {
+    // K2 completes only after K1 (the next kernel on the stream depends on K2 alone, and K1's
+    // last CTAs still reset the work counter), then advances the partial epoch
+    grid_dep_wait();
+    if (tid == 0) CHSET(stamp, 5);
+    if (tid == 0) P.ctrs[2] = stamp;
   }
 }
 
@@ -1650,6 +1794,7 @@ __global__ void __launch_bounds__(kFoldRows) lopa_fold_kernel(const Params P) {
     __syncthreads();
   }
   grid_dep_wait();
+  const uint32_t stamp = P.ctrs[2];  // K1 (complete) stamped its partials and advanced the epoch
   FoldAcc f;
   if (staged) {
     if (threadIdx.x == 0) {
@@ -1661,19 +1806,23 @@ __global__ void __launch_bounds__(kFoldRows) lopa_fold_kernel(const Params P) {
     }
     mbar_wait(bar, 0);
     float4 qr[16];
+    uint32_t bad = 0;
 #pragma unroll
-    for (int p = 0; p < 16; ++p) qr[p] = st[p * kFoldRows + threadIdx.x];
-#ifdef LOPA_CHECKED
-    if (valid)
-      for (int p = 0; p < P.n_grp; ++p) LOPA_CHK(__float_as_uint(qr[p].w) == P.epoch, 10);
-#endif
+    for (int p = 0; p < 16; ++p) {
+      uint32_t sp = stamp;
+      qr[p] = p < P.n_grp ? decode_slot(st[p * kFoldRows + threadIdx.x], &sp) : st[p * kFoldRows + threadIdx.x];
+      bad |= sp != stamp;
+    }
+    if (valid) LOPA_CHK(!bad, 10);
+    (void)bad;
     f = fold_tree16(16, qr);
   } else if (valid) {
-#ifdef LOPA_CHECKED
-    for (int p = 0; p < P.n_grp; ++p)
-      LOPA_CHK(__float_as_uint(__ldcg(P.gpart + r + (size_t)p * P.n_cand).w) == P.epoch, 10);
-#endif
-    f = fold_row_global(P.gpart + r, P.n_grp, (size_t)P.n_cand);
+    f = fold_seq(P.n_grp, [&](int p) {
+      uint64_t A, B;
+      load_partial_raw(P.gpart + r + (size_t)p * P.n_cand, &A, &B);
+      LOPA_CHK(stamped(A, B, stamp), 10);
+      return decode_partial(A, B);
+    });
   }
   if (valid) {
     P.conf[r] = __fdiv_rn(1.0f, f.S);
@@ -2011,10 +2160,7 @@ static int launch_reduce(const Params& P0, int device, cudaStream_t s, bool k1_o
   int st = ensure_kernel_attrs(device);
   if (st != LOPA_OK) return st;
   Params P = P0;
-#ifdef LOPA_CHECKED
-  static std::atomic<uint32_t> g_epoch{0};
-  P.epoch = 1u + (g_epoch.fetch_add(1u) & 0x3FFFFFFFu);  // never 0: a zeroed workspace never matches
-#endif
+  P.k1_alone = k1_only ? 1 : 0;
   if (k1_only) {  // measurement: K1 alone, in the step's launch configuration
     const int g = kK1CtasPerSm * (num_sms(device) - 1);
     return cuda_status(launch_pdl(LOPA_K1_KERNEL, dim3(g), dim3(kK1Threads), kK1Smem, s, P));
@@ -2245,6 +2391,24 @@ extern "C" int lopa_debug_timeline(unsigned long long* out, int n_ctas) {
   return lopa::kTlSlots;
 #else
   (void)out; (void)n_ctas;
+  return 0;
+#endif
+}
+
+// Debug (LOPA_CHAIN_TL builds): per-step marks of chained steps ([64][8] ns), then cleared.
+extern "C" int lopa_debug_chain_timeline(unsigned long long* out, int n_words) {
+#ifdef LOPA_CHAIN_TL
+  const int need = 64 * 8;
+  if (!out || n_words < need) return -need;
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, lopa::g_chain, sizeof(lopa::g_chain)) != cudaSuccess) return 0;
+  unsigned long long init[64][8];
+  for (int i = 0; i < 64; ++i)
+    for (int j = 0; j < 8; ++j) init[i][j] = (j == 0 || j == 6) ? ~0ull : 0ull;
+  cudaMemcpyToSymbol(lopa::g_chain, init, sizeof(init));
+  return need;
+#else
+  (void)out; (void)n_words;
   return 0;
 #endif
 }

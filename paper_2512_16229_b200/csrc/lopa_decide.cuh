@@ -16,6 +16,7 @@ namespace lopa {
 constexpr int kDevEmptyMask = 1;
 constexpr int kDevNonfinite = 2;
 constexpr int kDevPeerTimeout = 4;
+constexpr int kDevInternal = 8;   // LOPA_DEV_INTERNAL: a K1 partial never arrived (bounded poll)
 
 // Position state of one window held in registers.
 template <int S>

@@ -103,6 +103,7 @@ _SIGS = {
     "lopa_debug_timeline": (_i32, [_c_void_p, _i32]),
     "lopa_debug_ldg_timeline": (_i32, [_c_void_p, _i32]),
     "lopa_debug_k1_timeline": (_i32, [_c_void_p, _i32]),
+    "lopa_debug_chain_timeline": (_i32, [_c_void_p, _i32]),
     "lopa_profile_enable": (_i32, [_i32]),
     "lopa_profile_read": (_i32, [ctypes.POINTER(ctypes.c_float), _i32, ctypes.POINTER(_i32)]),
     "lopa_syn_generate": (_i32, [_u64, _i32, _i32, _i64, _i32, _i32, _c_void_p, _c_void_p, _i32,
