@@ -239,6 +239,12 @@ __device__ __forceinline__ void mask_tail(uint4& v, int nvalid) {
 // (lo - m, hi - m) of a bf16x2 word, each formed exactly as one fp32 rounding of x - m:
 // fma.rn.f32.bf16 reads the bf16 halves in place (FHFMA.BF16: no unpack instructions).
 __device__ __forceinline__ float2 minus_m(uint32_t w, float negm) {
+#ifdef LOPA_MINUS_M_UNPACK
+  // experiment: unpack the halves on the integer pipe, one packed fp32 add (the same single
+  // rounding of x - m, so the same bits)
+  return __fadd2_rn(make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u)),
+                    make_float2(negm, negm));
+#endif
   float lo, hi;
   asm("{\n.reg .b16 l, h, one;\n"
       "mov.b32 {l, h}, %2;\n"
