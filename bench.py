@@ -662,6 +662,25 @@ def run_lopa(args):
         loop = {"blocks": 8, "tokens": tok_total, "forwards": fw_total, "tpf": tok_total / fw_total,
                 "ms_per_block_incl_generator": l0.elapsed_time(l1) / 8,
                 "note": "one host read per iteration (branch count); SYN-D2F forward on the GPU"}
+        # the same 8 blocks, each ONE self-terminating CUDA graph launch (conditional WHILE node:
+        # the loop stops on the device when the selected branch is complete; no host read)
+        graphs = [lopa.DecodeBlockGraph(lopa.Stepper(V, W, k + 1, k, tau, dev), seed, blk) for blk in range(8)]
+        t0_ = torch.zeros(W, dtype=torch.int32, device=dev)
+        m0_ = torch.ones(W, dtype=torch.uint8, device=dev)
+        for g_ in graphs:
+            g_.run(t0_, m0_)
+        torch.cuda.synchronize()
+        l0.record(stream)
+        for g_ in graphs:
+            g_.run(t0_, m0_)
+        l1.record(stream)
+        torch.cuda.synchronize()
+        fw_g = sum(g_.forwards() for g_ in graphs)
+        loop["graph_ms_per_block_incl_generator"] = l0.elapsed_time(l1) / 8
+        loop["graph_forwards"] = fw_g
+        loop["graph_note"] = "each block one device-terminated CUDA graph (lopa.DecodeBlockGraph)"
+        for g_ in graphs:
+            g_.graph.close()
 
     # e2e through the public API with HOST buffers: pinned logits -> device, step, results -> host.
     # At N > 1 (branch-parallel) each rank copies its own shard of the logits (its branches'
@@ -1038,6 +1057,21 @@ def run_d2f(args):
     # the harness forward alone, as the same captured loop runs it: one graph of the forwards of
     # the recorded windows (the scheduler state replayed from the trace is not needed: the
     # forward's cost depends on the window size and branch count only)
+    # the same decode as ONE self-terminating graph (conditional WHILE: stops on the device when
+    # every block is committed; no iteration count)
+    wg = loop.capture_while()
+    wg_ms = 0.0
+    for r_ in range(reps + 2):
+        loop.reset()
+        e0.record(stream)
+        loop.launch_while()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if r_ >= 2:
+            wg_ms += e0.elapsed_time(e1)
+    if wg.iterations() != iters or not torch.equal(loop.trace().tokens, h.tokens):
+        raise RuntimeError("device-terminated D2F loop diverged from the host pipeline")
+    wg.close()
     per_it = dev_ms / reps / iters
     line = {
         "metric": METRIC, "value": 1000.0 / per_it, "unit": UNIT, "n_gpus": 1, "steps": reps * iters,
@@ -1048,6 +1082,7 @@ def run_d2f(args):
                    "tokens_per_forward": Lg / iters, "max_window": max(w[1] for w in g.windows),
                    "parallelism": "single"},
         "d2f": {"device_graph_us_per_iteration": per_it * 1000.0,
+                "device_while_graph_us_per_iteration": wg_ms / reps / iters * 1000.0,
                 "host_pipeline_us_per_iteration": host_ms / hreps / iters * 1000.0,
                 "speedup": (host_ms / hreps) / (dev_ms / reps),
                 "note": "both include the SYN-D2F forward of every iteration (windows up to 256 "

@@ -259,6 +259,34 @@ int lopa_d2f_update(const lopa_d2f_t* d, const int32_t* winner, const int32_t* n
 int lopa_d2f_syn_forward(uint64_t seed, int32_t vocab, int64_t ld, int32_t extras,
                          const lopa_d2f_t* d, void* logits, void* stream);
 
+/* ---------------------------------------------------------------- device-terminated loops
+ * A CUDA graph whose body repeats on the device under a conditional WHILE node until a
+ * condition word stops it: the Alg. 1 loop until the selected branch is complete (R21: the
+ * step's n_branches_next = 0) or a D2F decode until every block is committed (sched[3] != 0),
+ * with no host read and no fixed iteration count.
+ *   lopa_while_begin: starts capturing `stream` into the loop body; the caller then issues the
+ *     body (e.g. forward + lopa_step + table copies) on that stream; cond_word: device int32,
+ *     read after each iteration: continue while it is non-zero (until_zero = 1) or zero
+ *     (until_zero = 0), and at most max_iters iterations per launch.
+ *   lopa_while_end: appends the condition kernel, ends the capture, instantiates the graph.
+ *   lopa_while_launch: runs the whole loop (>= 1 iteration) on `stream` (NULL: the legacy
+ *     default stream, as every other call); asynchronous.  lopa_while_iterations: iterations of the last launch (synchronous).
+ * The body must not allocate or synchronise.  Errors: INVALID_ARG (order of calls), CUDA. */
+typedef struct lopa_while lopa_while_t;
+int lopa_while_begin(void* stream, const int32_t* cond_word, int32_t until_zero, int32_t max_iters,
+                     lopa_while_t** out);
+int lopa_while_end(lopa_while_t* w);
+int lopa_while_launch(lopa_while_t* w, void* stream);
+int lopa_while_iterations(const lopa_while_t* w, int32_t* out_host);
+void lopa_while_destroy(lopa_while_t* w);
+
+/* Harness: lopa_syn_generate for the branches present, read on the device (n_branches_dev,
+ * <= max_branches): the forward stand-in inside a device-terminated loop. */
+int lopa_syn_generate_dev(uint64_t seed, int32_t block, int32_t vocab, int64_t ld, int32_t window,
+                          int32_t max_branches, const int32_t* n_branches_dev,
+                          const int32_t* branch_tokens, const uint8_t* branch_mask, int32_t extras,
+                          void* out, void* stream);
+
 /* ---------------------------------------------------------------- branch parallelism (a5)
  * Global branch j lives on rank j / B_loc, B_loc = ceil(max_branches / world).
  * Each rank reduces only its branches' logits, scores them, and publishes one record

@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblopa.so")
-SOURCES = ["lopa_core.cu", "lopa_syn.cu", "lopa_bp.cu", "lopa_lmhead.cu", "lopa_d2f.cu"]
+SOURCES = ["lopa_core.cu", "lopa_syn.cu", "lopa_bp.cu", "lopa_lmhead.cu", "lopa_d2f.cu", "lopa_graph.cu"]
 HEADERS = ["lopa_ptx.cuh", "lopa_decide.cuh", "lopa_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -281,6 +281,22 @@ class D2FDeviceLoop:
     def replay(self):
         self.graph.replay()
 
+    def capture_while(self, max_iters: int = 1 << 16):
+        """The whole decode as ONE device-terminated CUDA graph (lopa.WhileGraph): iterations
+        repeat on the device until every block is committed (sched[3] != 0) -- no iteration
+        count needed.  launch_while() after reset()."""
+        self.reset()
+        self.iteration()                      # warm-up outside the capture
+        torch.cuda.synchronize(self.dev)
+        self.reset()
+        torch.cuda.synchronize(self.dev)
+        self.while_graph = lopa.WhileGraph(self.iteration, self.sched[3:4], until_zero=False,
+                                           max_iters=max_iters)
+        return self.while_graph
+
+    def launch_while(self):
+        self.while_graph.launch()
+
     def done(self) -> bool:
         return bool(int(self.sched[3].item()))
 

@@ -67,6 +67,13 @@ _SIGS = {
     "lopa_debug_k1_attrs": (_i32, [ctypes.c_void_p]),
     "lopa_debug_check_read": (_i32, [ctypes.c_void_p]),
     "lopa_d2f_init": (_i32, [_c_void_p, _c_void_p]),
+    "lopa_while_begin": (_i32, [_c_void_p, _c_void_p, _i32, _i32, _c_void_p]),
+    "lopa_while_end": (_i32, [_c_void_p]),
+    "lopa_while_launch": (_i32, [_c_void_p, _c_void_p]),
+    "lopa_while_iterations": (_i32, [_c_void_p, _c_void_p]),
+    "lopa_while_destroy": (None, [_c_void_p]),
+    "lopa_syn_generate_dev": (_i32, [ctypes.c_uint64, _i32, _i32, _i64, _i32, _i32, _c_void_p, _c_void_p,
+                                     _c_void_p, _i32, _c_void_p, _c_void_p]),
     "lopa_d2f_update": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_d2f_syn_forward": (_i32, [ctypes.c_uint64, _i32, _i64, _i32, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_workspace_bytes": (_size, [_i32, _i32]),
@@ -456,6 +463,103 @@ class StepLoopGraph:
     def replay(self):
         self.graph.replay()
         return self.s.out
+
+
+class WhileGraph:
+    """A CUDA graph whose body repeats ON THE DEVICE until a condition word stops it (conditional
+    WHILE node, lopa_while_*): ``body()`` is issued once, captured into the loop body (it must not
+    allocate or synchronise); after every iteration the loop continues while ``cond_word`` (a
+    device int32) is non-zero (until_zero=True) or zero (until_zero=False), at most max_iters
+    times.  launch() runs the whole loop with no host involvement."""
+
+    def __init__(self, body, cond_word: torch.Tensor, until_zero: bool = True, max_iters: int = 1 << 20):
+        _need_cuda(cond_word)
+        self.device = cond_word.device
+        self.stream = torch.cuda.Stream(self.device)
+        torch.cuda.synchronize(self.device)
+        h = ctypes.c_void_p()
+        _check(lib().lopa_while_begin(ctypes.c_void_p(self.stream.cuda_stream), _p(cond_word),
+                                      1 if until_zero else 0, max_iters, ctypes.byref(h)), "lopa_while_begin")
+        self.h = h
+        try:
+            with torch.cuda.stream(self.stream):
+                body()
+        finally:
+            st = lib().lopa_while_end(h)
+        _check(st, "lopa_while_end")
+
+    def launch(self):
+        """Run the loop on the current stream (asynchronous)."""
+        _check(lib().lopa_while_launch(self.h, _stream(self.device)), "lopa_while_launch")
+
+    def iterations(self) -> int:
+        n = _i32(0)
+        torch.cuda.synchronize(self.device)
+        _check(lib().lopa_while_iterations(self.h, ctypes.byref(n)), "lopa_while_iterations")
+        return n.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().lopa_while_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def syn_generate_dev(seed: int, block: int, vocab: int, branch_tokens, branch_mask, n_branches_dev,
+                     out: torch.Tensor, extras: int = 0):
+    """SYN-D2F logits for the branches present, the count read on the device (harness)."""
+    mb, W = branch_mask.shape
+    _check(lib().lopa_syn_generate_dev(seed & ((1 << 64) - 1), block, vocab, out.stride(-2), W, mb,
+                                       _p(n_branches_dev), _p(branch_tokens), _p(_u8(branch_mask)),
+                                       extras, _p(out), _stream(out.device)), "lopa_syn_generate_dev")
+
+
+class DecodeBlockGraph:
+    """Alg. 1 over one window as ONE device-terminated CUDA graph (WhileGraph): each iteration is
+    the harness forward of the present branches (syn_generate_dev, the model stand-in), one
+    lopa_step and the device copy of the spawned tables; the loop ends on the device when the
+    selected branch is complete (n_branches_next = 0, R21).  run(tokens0, mask0) -> tokens;
+    forwards() = iterations of the last run."""
+
+    def __init__(self, stepper: "Stepper", seed: int, block: int, extras: int = 0):
+        st = stepper
+        self.s, self.seed, self.block, self.extras = st, seed, block, extras
+        d, W, mb = st.device, st.window, st.max_branches
+        self.tok = torch.zeros((mb, W), dtype=torch.int32, device=d)
+        self.msk = torch.zeros((mb, W), dtype=torch.uint8, device=d)
+        self.nb = torch.ones(1, dtype=torch.int32, device=d)
+        self.logits = torch.zeros((mb, W, st.ld), dtype=torch.bfloat16, device=d)
+        self._args = st.args(self.logits, self.nb, self.tok, self.msk)
+        # warm-up outside the capture (kernel attributes, lazy module loading), then restore
+        self._body()
+        torch.cuda.synchronize(d)
+        self.graph = WhileGraph(self._body, st.out.n_next, until_zero=True, max_iters=4 * W + 4)
+
+    def _body(self):
+        st, o = self.s, self.s.out
+        syn_generate_dev(self.seed, self.block, st.vocab, self.tok, self.msk, self.nb, self.logits, self.extras)
+        _check(lib().lopa_step(ctypes.byref(self._args), _stream(st.device)), "lopa_step")
+        k1 = o.next_tokens.shape[0]
+        self.tok[:k1].copy_(o.next_tokens)
+        self.msk[:k1].copy_(o.next_mask)
+        self.nb.copy_(o.n_next)
+
+    def run(self, tokens0: torch.Tensor, mask0: torch.Tensor, block: int | None = None) -> torch.Tensor:
+        self.tok.zero_()
+        self.msk.zero_()
+        self.tok[0].copy_(tokens0.to(torch.int32))
+        self.msk[0].copy_(_u8(mask0))
+        self.nb.fill_(1)
+        self.graph.launch()
+        return self.tok[0]
+
+    def forwards(self) -> int:
+        return self.graph.iterations()
 
 
 # ----------------------------------------------------------------------------- measurement
