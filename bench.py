@@ -967,6 +967,92 @@ def run_loop(args):
     h2d = sum(b.numel() * 2 for b in host0) / len(host0)
     d2h = sum(t.numel() * t.element_size() for t in h_out)
 
+    # the recorded trajectory replayed as ONE static CUDA graph (the step count of every block from
+    # the recording; no host read): the device time of the LoPA loop itself on resident logits
+    graph_replay = None
+    if not getattr(drv, "p2p", False):
+        def replay_all():
+            for blk in range(nblk):
+                tok.zero_()
+                msk.zero_()
+                msk[0].fill_(1)
+                nb.fill_(1)
+                for si in range(fw_blocks[blk]):
+                    out = drv.step(padded[blk][si], nb, tok, msk)
+                    tok.copy_(out.next_tokens)
+                    msk.copy_(out.next_mask)
+                    nb.copy_(out.n_next)
+        replay_all()
+        torch.cuda.synchronize()
+        cgr = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(cgr, stream=cs):
+                replay_all()
+        torch.cuda.synchronize()
+        for _ in range(2):
+            cgr.replay()
+        torch.cuda.synchronize()
+        if int(st.out.n_next.item()) != 0:
+            raise RuntimeError("graph replay did not end its last block")
+        reps_g = max(2, min(20, K // max(1, steps_per_pass)))
+        if dist:
+            dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(reps_g):
+            cgr.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gr_ms = g0.elapsed_time(g1)
+        if dist:
+            t = torch.tensor([gr_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            gr_ms = float(t.item())
+        graph_replay = {"us_per_step": gr_ms * 1000.0 / (reps_g * steps_per_pass),
+                        "verify_steps_per_s": reps_g * steps_per_pass / (gr_ms / 1000.0),
+                        "passes": reps_g,
+                        "note": "the recorded loop (every step's resident logits shard, tables fed "
+                                "back on the device, block starts reset on the device) as one static "
+                                "CUDA graph; the step counts come from the recording pass"}
+        del cgr
+
+    # the same decode with each block ONE device-terminated CUDA graph (conditional WHILE node;
+    # no host read at all; the SYN-D2F forward of this rank's branches inside the loop)
+    dev_loop = None
+    if not getattr(drv, "p2p", False):
+        graphs = [(lopa.DecodeBlockGraphBP(drv, seed, blk) if use_bp else lopa.DecodeBlockGraph(st, seed, blk))
+                  for blk in range(nblk)]
+        t0_ = torch.zeros(W, dtype=torch.int32, device=dev)
+        m0_ = torch.ones(W, dtype=torch.uint8, device=dev)
+        for g_ in graphs:
+            g_.run(t0_, m0_)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for g_ in graphs:
+            g_.run(t0_, m0_)
+        d1.record(stream)
+        torch.cuda.synchronize()
+        dl_ms = d0.elapsed_time(d1)
+        if dist:
+            t = torch.tensor([dl_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dl_ms = float(t.item())
+        fw_dl = [g_.forwards() for g_ in graphs]
+        if fw_dl != fw_blocks:
+            raise RuntimeError(f"device-terminated loop diverged: {fw_dl} vs {fw_blocks}")
+        dev_loop = {"us_per_step_incl_forward": dl_ms * 1000.0 / steps_per_pass,
+                    "ms_per_pass": dl_ms, "forwards_per_block": fw_dl,
+                    "note": "each block one device-terminated CUDA graph (lopa.DecodeBlockGraph"
+                            + ("BP, NCCL all-gather inside the graph" if use_bp else "") +
+                            "): no host read; includes the SYN-D2F forward of this rank's branches"}
+        for g_ in graphs:
+            g_.graph.close()
+
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
@@ -993,6 +1079,10 @@ def run_loop(args):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if dev_loop is not None:
+            line["device_loop"] = dev_loop
+        if graph_replay is not None:
+            line["graph_replay"] = graph_replay
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()  # rank 0's CPU baseline runs while the others wait here

@@ -280,10 +280,12 @@ int lopa_while_launch(lopa_while_t* w, void* stream);
 int lopa_while_iterations(const lopa_while_t* w, int32_t* out_host);
 void lopa_while_destroy(lopa_while_t* w);
 
-/* Harness: lopa_syn_generate for the branches present, read on the device (n_branches_dev,
- * <= max_branches): the forward stand-in inside a device-terminated loop. */
+/* Harness: lopa_syn_generate for the branches present, the count read on the device: branch
+ * tables (and out) hold the shard of global branches [branch_base, branch_base + max_branches);
+ * rows of global branches >= *n_branches_dev are skipped.  The forward stand-in inside a
+ * device-terminated loop (branch_base = 0 on one GPU, the rank's first branch under BP). */
 int lopa_syn_generate_dev(uint64_t seed, int32_t block, int32_t vocab, int64_t ld, int32_t window,
-                          int32_t max_branches, const int32_t* n_branches_dev,
+                          int32_t max_branches, const int32_t* n_branches_dev, int32_t branch_base,
                           const int32_t* branch_tokens, const uint8_t* branch_mask, int32_t extras,
                           void* out, void* stream);
 

@@ -119,10 +119,11 @@ __global__ void syn_kernel(uint64_t seed, int blk, int V, long long ld, int W, i
 // lopa_syn_generate with the branch count read on the device: grid (W, max_branches), rows of
 // absent branches (j >= *n) skip.
 __global__ void syn_dev_kernel(uint64_t seed, int blk, int V, long long ld, int W, int c8,
-                               const int32_t* __restrict__ n_dev, const int32_t* __restrict__ br_tok,
+                               const int32_t* __restrict__ n_dev, int base,
+                               const int32_t* __restrict__ br_tok,
                                const uint8_t* __restrict__ br_msk, int extras, uint16_t* __restrict__ out) {
   const int i = blockIdx.x, j = blockIdx.y;
-  if (j >= *n_dev) return;
+  if (j >= *n_dev - base) return;  // branches [base, n) present: this shard's rows j < n - base
   syn_row(seed, blk, V, ld, W, c8, br_tok + (size_t)j * W, br_msk + (size_t)j * W, i, extras,
           out + ((size_t)j * W + i) * (size_t)ld);
 }
@@ -188,9 +189,10 @@ extern "C" int lopa_d2f_syn_forward(uint64_t seed, int32_t vocab, int64_t ld, in
 
 extern "C" int lopa_syn_generate_dev(uint64_t seed, int32_t block, int32_t vocab, int64_t ld,
                                      int32_t window, int32_t max_branches, const int32_t* n_branches_dev,
-                                     const int32_t* branch_tokens, const uint8_t* branch_mask,
-                                     int32_t extras, void* out, void* stream) {
-  if (vocab < 1 || ld < vocab || ld % 8 != 0 || window < 1 || max_branches < 1 || block < 0)
+                                     int32_t branch_base, const int32_t* branch_tokens,
+                                     const uint8_t* branch_mask, int32_t extras, void* out, void* stream) {
+  if (vocab < 1 || ld < vocab || ld % 8 != 0 || window < 1 || max_branches < 1 || block < 0 ||
+      branch_base < 0)
     return LOPA_ERR_INVALID_ARG;
   if (!n_branches_dev || !branch_tokens || !branch_mask || !out || (reinterpret_cast<uintptr_t>(out) & 15))
     return LOPA_ERR_INVALID_ARG;
@@ -200,7 +202,7 @@ extern "C" int lopa_syn_generate_dev(uint64_t seed, int32_t block, int32_t vocab
   const int c8 = vocab < 2 ? 0 : (int)std::lround(8.0 * std::log(1.8 * (double)(vocab - 1)));
   dim3 grid(window, max_branches);
   lopa::syn::syn_dev_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      seed, block, vocab, ld, window, c8, n_branches_dev, branch_tokens, branch_mask, extras,
-      static_cast<uint16_t*>(out));
+      seed, block, vocab, ld, window, c8, n_branches_dev, branch_base, branch_tokens, branch_mask,
+      extras, static_cast<uint16_t*>(out));
   return lopa::cuda_status(cudaGetLastError());
 }

@@ -72,8 +72,8 @@ _SIGS = {
     "lopa_while_launch": (_i32, [_c_void_p, _c_void_p]),
     "lopa_while_iterations": (_i32, [_c_void_p, _c_void_p]),
     "lopa_while_destroy": (None, [_c_void_p]),
-    "lopa_syn_generate_dev": (_i32, [ctypes.c_uint64, _i32, _i32, _i64, _i32, _i32, _c_void_p, _c_void_p,
-                                     _c_void_p, _i32, _c_void_p, _c_void_p]),
+    "lopa_syn_generate_dev": (_i32, [ctypes.c_uint64, _i32, _i32, _i64, _i32, _i32, _c_void_p, _i32,
+                                     _c_void_p, _c_void_p, _i32, _c_void_p, _c_void_p]),
     "lopa_d2f_update": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_d2f_syn_forward": (_i32, [ctypes.c_uint64, _i32, _i64, _i32, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_workspace_bytes": (_size, [_i32, _i32]),
@@ -511,12 +511,14 @@ class WhileGraph:
 
 
 def syn_generate_dev(seed: int, block: int, vocab: int, branch_tokens, branch_mask, n_branches_dev,
-                     out: torch.Tensor, extras: int = 0):
-    """SYN-D2F logits for the branches present, the count read on the device (harness)."""
+                     out: torch.Tensor, extras: int = 0, branch_base: int = 0):
+    """SYN-D2F logits for the branches present, the count read on the device (harness); the
+    tables / out hold global branches [branch_base, branch_base + rows)."""
     mb, W = branch_mask.shape
     _check(lib().lopa_syn_generate_dev(seed & ((1 << 64) - 1), block, vocab, out.stride(-2), W, mb,
-                                       _p(n_branches_dev), _p(branch_tokens), _p(_u8(branch_mask)),
-                                       extras, _p(out), _stream(out.device)), "lopa_syn_generate_dev")
+                                       _p(n_branches_dev), branch_base, _p(branch_tokens),
+                                       _p(_u8(branch_mask)), extras, _p(out), _stream(out.device)),
+           "lopa_syn_generate_dev")
 
 
 class DecodeBlockGraph:
@@ -560,6 +562,44 @@ class DecodeBlockGraph:
 
     def forwards(self) -> int:
         return self.graph.iterations()
+
+
+class DecodeBlockGraphBP:
+    """DecodeBlockGraph branch-parallel: this rank's iteration = the harness forward of ITS OWN
+    present branches (syn_generate_dev on global branches [lo, hi), count read on the device),
+    lopa_bp_step (local reduction and record, the NCCL all-gather, the replicated select /
+    anchor / spawn) and the table copies, in one device-terminated graph per block (every rank
+    holds the same tables, so every rank's loop stops at the same iteration).  NCCL path only:
+    the peer-memory exchange keeps its epoch on the host and is not graph-capturable."""
+
+    def __init__(self, bp: "BranchParallel", seed: int, block: int, extras: int = 0):
+        if bp.p2p:
+            raise LopaError("DecodeBlockGraphBP needs the NCCL exchange (p2p=False)")
+        st = bp.s
+        self.bp, self.s, self.seed, self.block, self.extras = bp, st, seed, block, extras
+        d, W, mb = st.device, st.window, st.max_branches
+        self.tok = torch.zeros((mb, W), dtype=torch.int32, device=d)
+        self.msk = torch.zeros((mb, W), dtype=torch.uint8, device=d)
+        self.nb = torch.ones(1, dtype=torch.int32, device=d)
+        _, self.lo, self.hi, self.local = bp.ranks()[0]
+        self._body()
+        torch.cuda.synchronize(d)
+        self.graph = WhileGraph(self._body, st.out.n_next, until_zero=True, max_iters=4 * W + 4)
+
+    def _body(self):
+        st, o = self.s, self.s.out
+        if self.hi > self.lo:
+            syn_generate_dev(self.seed, self.block, st.vocab, self.tok[self.lo:self.hi],
+                             self.msk[self.lo:self.hi], self.nb, self.local[: self.hi - self.lo],
+                             self.extras, branch_base=self.lo)
+        self.bp.step(self.local, self.nb, self.tok, self.msk)
+        k1 = o.next_tokens.shape[0]
+        self.tok[:k1].copy_(o.next_tokens)
+        self.msk[:k1].copy_(o.next_mask)
+        self.nb.copy_(o.n_next)
+
+    run = DecodeBlockGraph.run
+    forwards = DecodeBlockGraph.forwards
 
 
 # ----------------------------------------------------------------------------- measurement

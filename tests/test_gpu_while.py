@@ -61,3 +61,29 @@ def test_d2f_while_graph(L):
         assert g.windows == h.windows and g.winners == h.winners and g.commits == h.commits
         assert torch.equal(g.tokens, h.tokens)
     wg.close()
+
+
+def test_bp_decode_block_graph_nccl_single_rank(L):
+    """The branch-parallel block loop (harness forward of the rank's branches, lopa_bp_step with
+    its NCCL all-gather, table copies) as one device-terminated graph, one rank: the configs[2]
+    blocks' tokens and forward counts equal the oracle's stored decode."""
+    import json
+    import os
+    c = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_decode_configs.json")))["dream_k15_256"]
+    st = L.Stepper(c["V"], c["W"], c["k"] + 1, c["k"], c["tau"], DEV)
+    bp = L.BranchParallel(st, 0, 1)
+    try:
+        toks, fws = [], []
+        for blk in range(3):
+            g = L.DecodeBlockGraphBP(bp, c["seed"], blk)
+            t = g.run(torch.zeros(c["W"], dtype=torch.int32, device=DEV),
+                      torch.ones(c["W"], dtype=torch.uint8, device=DEV)).clone()
+            torch.cuda.synchronize()
+            toks.extend(t.cpu().tolist())
+            fws.append(g.forwards())
+            g.graph.close()
+        bp.check()
+    finally:
+        bp.close()
+    assert fws == c["forwards_per_block"][:3]
+    assert toks == c["tokens"][: 3 * c["W"]]
