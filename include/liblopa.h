@@ -39,9 +39,11 @@
  *   - Branch tables are [max_branches][window] row-major; branch 0 is the anchor B0.
  *   - tau is fp32; a position is "high" iff (float)conf > tau (strict; R5, R14).
  *   - Workspace: lopa_workspace_bytes() bytes of device memory, zeroed by the caller ONCE
- *     before first use; every successful call leaves its counters zero again.  A workspace
- *     must not be used by two calls that may run concurrently.  After a LOPA_ERR_CUDA
- *     return, zero it again.
+ *     before first use; the library keeps its state there (every successful call leaves the
+ *     work counters zero again and advances the partial epoch that tells the reduction's
+ *     partials of this call from stale ones), so it may be shared by every kind
+ *     of call and by CUDA-graph replays.  A workspace must not be used by two calls that may
+ *     run concurrently.  After a LOPA_ERR_CUDA return, zero it again.
  */
 #ifndef LIBLOPA_H_
 #define LIBLOPA_H_

@@ -177,7 +177,8 @@ def workspace_bytes(max_rows: int, vocab: int) -> int:
 
 
 def new_workspace(max_rows: int, vocab: int, device) -> torch.Tensor:
-    """Zeroed device workspace (zero once; the kernels leave it zeroed)."""
+    """Zeroed device workspace (zero once before first use; the library keeps its counters and
+    the partial epoch in it, liblopa.h conventions)."""
     return torch.zeros(workspace_bytes(max_rows, vocab), dtype=torch.uint8, device=device)
 
 
