@@ -362,7 +362,7 @@ int lopa_debug_ldg_timeline(unsigned long long* out, int n_words);
 /* Debug: per-item timeline of the TMA-form K1's last launch (-DLOPA_K1_TL builds only); same
  * return convention. */
 int lopa_debug_k1_timeline(unsigned long long* out, int n_words);
-/* Debug: per-step marks of chained steps (-DLOPA_CHAIN_TL builds only), [64][8] ns; cleared. */
+/* Debug: per-step marks of chained steps (-DLOPA_CHAIN_TL builds only), [64][12] ns; cleared. */
 int lopa_debug_chain_timeline(unsigned long long* out, int n_words);
 
 /* ---------------------------------------------------------------- harness (not the method)

@@ -97,6 +97,24 @@ __device__ __noinline__ void chk_fail(int site) {
 #else
 #define LOPA_CHK(cond, site) ((void)0)
 #endif
+#ifdef LOPA_CHAIN_TL
+// experiment: per-step %globaltimer marks of chained steps, indexed by the partial epoch:
+// [epoch % 64][0 K1 first CTA start, 1 K1 last CTA end, 2 K2 start, 3 K2 rows folded,
+//  4 K2 decisions done, 5 K2 final wait returned, 6 K1 first CTA after its wait]
+__device__ unsigned long long g_chain[64][12];
+__device__ __forceinline__ unsigned long long ch_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CHMIN(e, s) atomicMin(&g_chain[(e) & 63][(s)], ch_now())
+#define CHMAX(e, s) atomicMax(&g_chain[(e) & 63][(s)], ch_now())
+#define CHSET(e, s) (g_chain[(e) & 63][(s)] = ch_now())
+#else
+#define CHMIN(e, s) ((void)0)
+#define CHMAX(e, s) ((void)0)
+#define CHSET(e, s) ((void)0)
+#endif
 }  // namespace lopa
 #include "lopa_decide.cuh"
 #include "lopa_internal.h"
@@ -558,6 +576,7 @@ struct TailSmem {
   float taus[LOPA_MAX_WINDOW];  // per-position thresholds (staged from P.tau_pos, if any)
   int32_t n;       // lookahead count, -1 = winner complete
   int32_t best;    // (BP) local best
+  uint32_t stamp;  // this launch's partial epoch (timeline builds' marks)
   double dscr[kScoreWarps][LOPA_MAX_WINDOW];  // per-warp metric scratch
   float fscr[kScoreWarps][LOPA_MAX_WINDOW];
 };
@@ -606,6 +625,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
   cta_scores<NT, S>(T, P, nb, W, warp, lane, P.scores);
   __syncthreads();
   if (tid == 0) TLC(22);
+  if (tid == 0) CHSET(T.stamp, 7);
   TL(7);
   if (warp >= S) return;
   constexpr int kPos = 32 * S;
@@ -644,6 +664,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
     }
   }
   named_bar_sync(1, kPos);
+  if (tid == 0) CHSET(T.stamp, 8);
   TL(9);
   const int nl = T.n;
   if (nl < 0) {  // R21: the winner is complete -> pass it through, no branches
@@ -672,6 +693,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
       for (int q = nl + tid; q < P.k; q += kPos) P.lookahead[q] = -1;
   }
   named_bar_sync(1, kPos);
+  if (tid == 0) CHSET(T.stamp, 9);
   TL(12);
   // next tables: thread = position i, rows j = 0..nl
   if (tid < W) {
@@ -687,6 +709,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
     }
   }
   if (tid == 0) *P.n_next = nl + 1;
+  if (tid == 0) CHSET(T.stamp, 10);
   TL(13);
 }
 
@@ -736,24 +759,6 @@ __device__ __forceinline__ unsigned long long k1_gtime() {
 #define K1TL(idx) (g_k1tl[blockIdx.x][(idx)] = k1_gtime())
 #else
 #define K1TL(idx) ((void)0)
-#endif
-#ifdef LOPA_CHAIN_TL
-// experiment: per-step %globaltimer marks of chained steps, indexed by the partial epoch:
-// [epoch % 64][0 K1 first CTA start, 1 K1 last CTA end, 2 K2 start, 3 K2 rows folded,
-//  4 K2 decisions done, 5 K2 final wait returned, 6 K1 first CTA after its wait]
-__device__ unsigned long long g_chain[64][8];
-__device__ __forceinline__ unsigned long long ch_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define CHMIN(e, s) atomicMin(&g_chain[(e) & 63][(s)], ch_now())
-#define CHMAX(e, s) atomicMax(&g_chain[(e) & 63][(s)], ch_now())
-#define CHSET(e, s) (g_chain[(e) & 63][(s)] = ch_now())
-#else
-#define CHMIN(e, s) ((void)0)
-#define CHMAX(e, s) ((void)0)
-#define CHSET(e, s) ((void)0)
 #endif
 // A work claim.  LOPA_TMA_ASM_ATOM: one atom instruction whose value is waited for where it is
 // used (atomicAdd is warp-aggregated by the compiler: vote + shuffle of the returned value,
@@ -845,11 +850,13 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     TL(1);
     // raw item b (no division on the common path: the kernel's first instructions are fetched
     // cold at every launch, and an integer-division subroutine there measured +0.35 us)
+#ifndef LOPA_NO_SPEC
     if (b < P.n_cand) {
       issue(0, b);
     } else if (b < n_items_cap) {
       issue(b / P.n_cand, b % P.n_cand);
     }
+#endif
     // the first two claims travel while the masks load
     if (dyn) {
       p1 = K1_CLAIM(&P.ctrs[0]);
@@ -894,8 +901,13 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     // (computed on the compact path only: no division on the common path, see above)
     int n_rows = P.n_cand, lo = 0, q = 0;
     if (compact) {
+#ifdef LOPA_NO_SPEC
+      q = 0;  // experiment: no speculative copy, so no raw item is covered
+      const int rq = 0;
+#else
       q = G / P.n_cand;  // n_cand > 0 here (compact implies 7 n_cand > 8 n_valid >= 0)
       const int rq = G - q * P.n_cand;
+#endif
       n_rows = n_valid;
       int base = 0;
 #pragma unroll 1
@@ -922,6 +934,9 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
           const int g = cur / P.n_cand, row = cur - g * P.n_cand;
           if (row_valid(row)) issue(g, row);
         };
+#ifdef LOPA_NO_SPEC
+        if (b < n_items) maybe_issue(b);  // experiment: item b only after the masks
+#endif
         for (int jr = 1; jr < S && jr * G + b < n_items; ++jr) maybe_issue(jr * G + b);
         if (dyn) {
           while (true) {
@@ -1756,7 +1771,10 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
 #endif
   if (tid == 0) TLC(18);
   __syncthreads();
-  if (tid == 0) { TL(7); TLC(19); CHSET(stamp, 3); }
+  if (tid == 0) { TL(7); TLC(19); CHSET(stamp, 3); T.stamp = stamp; }
+#ifdef LOPA_CHAIN_TL
+  __syncthreads();
+#endif
   if (MODE == MODE_STEP || MODE == MODE_DECIDE) cta_tail_step<kTailThreads, S>(P, T, tid, nb);
   if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads, S>(P, T, tid, nb);
   if (tid == 0) {
@@ -2404,13 +2422,13 @@ extern "C" int lopa_debug_timeline(unsigned long long* out, int n_ctas) {
 // Debug (LOPA_CHAIN_TL builds): per-step marks of chained steps ([64][8] ns), then cleared.
 extern "C" int lopa_debug_chain_timeline(unsigned long long* out, int n_words) {
 #ifdef LOPA_CHAIN_TL
-  const int need = 64 * 8;
+  const int need = 64 * 12;
   if (!out || n_words < need) return -need;
   cudaDeviceSynchronize();
   if (cudaMemcpyFromSymbol(out, lopa::g_chain, sizeof(lopa::g_chain)) != cudaSuccess) return 0;
-  unsigned long long init[64][8];
+  unsigned long long init[64][12];
   for (int i = 0; i < 64; ++i)
-    for (int j = 0; j < 8; ++j) init[i][j] = (j == 0 || j == 6) ? ~0ull : 0ull;
+    for (int j = 0; j < 12; ++j) init[i][j] = (j == 0 || j == 6) ? ~0ull : 0ull;
   cudaMemcpyToSymbol(lopa::g_chain, init, sizeof(init));
   return need;
 #else

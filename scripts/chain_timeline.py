@@ -13,24 +13,24 @@ from paper_2512_16229_b200 import lopa  # noqa: E402
 dev = torch.device("cuda:0")
 st, tok, msk, nb, full, bufs, rows, _ = bench.build_workload(lopa, dev, 151936, 32, 7, 0.9, 1, 8)
 L = lopa.lib()
-buf = np.zeros(512, dtype=np.uint64)
-L.lopa_debug_chain_timeline(buf.ctypes.data, 512)   # clear
+buf = np.zeros(768, dtype=np.uint64)
+L.lopa_debug_chain_timeline(buf.ctypes.data, 768)   # clear
 argv = [st.args(b, nb, tok, msk) for b in bufs]
 s = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 for i in range(10):
     L.lopa_step(ctypes.byref(argv[i % 8]), s)
 torch.cuda.synchronize()
-L.lopa_debug_chain_timeline(buf.ctypes.data, 512)   # clear again
+L.lopa_debug_chain_timeline(buf.ctypes.data, 768)   # clear again
 bench.head_start(torch.cuda.current_stream(dev))
 for i in range(40):
     L.lopa_step(ctypes.byref(argv[i % 8]), s)
 torch.cuda.synchronize()
-L.lopa_debug_chain_timeline(buf.ctypes.data, 512)
-a = buf.reshape(64, 8).astype(np.int64)
+L.lopa_debug_chain_timeline(buf.ctypes.data, 768)
+a = buf.reshape(64, 12).astype(np.int64)
 ok = [e for e in range(64) if a[e, 1] > 0 and a[e, 5] > 0 and a[e, 6] < (1 << 62)]
 ok.sort(key=lambda e: a[e, 6])
-names = ["K1 start(wait done)", "K1 end", "K2 start", "K2 folded", "K2 decided", "K2 wait ret"]
-cols = [6, 1, 2, 3, 4, 5]
+names = ["K1 start(wait done)", "K1 end", "K2 start", "K2 folded", "scores", "anchor", "ranks", "tables", "K2 decided", "K2 wait ret"]
+cols = [6, 1, 2, 3, 7, 8, 9, 10, 4, 5]
 base = a[ok[0], 6]
 print("step | " + " | ".join(names) + " | period (us)")
 prev = None
