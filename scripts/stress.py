@@ -11,6 +11,17 @@ import _gpu as G
 from paper_2512_16229_b200 import lopa
 
 dev = "cuda:0"
+
+
+def _checked_violations():
+    """Violations counted by a -DLOPA_CHECKED build (LOPA_LIB_VARIANT=checked), else 0."""
+    import ctypes
+    out = (ctypes.c_uint32 * 3)()
+    st = lopa.lib().lopa_debug_check_read(ctypes.cast(out, ctypes.c_void_p))
+    if st == 0 and out[0]:
+        raise AssertionError(f"checked build: {out[0]} violations, first site {out[1]}, sites {out[2]:#x}")
+    return st == 0
+
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 t0, n_cases, n_steps = time.time(), 0, 0
@@ -56,4 +67,7 @@ while time.time() - t0 < budget:
             break
         tok, msk, nb = out.next_tokens.clone(), out.next_mask.clone(), out.n_next.clone()
     n_cases += 1
-print(f"stress ok: {n_cases} cases, {n_steps} steps in {time.time() - t0:.0f} s", flush=True)
+    if n_cases % 50 == 0:
+        _checked_violations()
+checked = _checked_violations()
+print(f"stress ok ({'checked build, 0 violations' if checked else 'product build'}): {n_cases} cases, {n_steps} steps in {time.time() - t0:.0f} s", flush=True)

@@ -11,6 +11,17 @@ import _gpu as G
 from paper_2512_16229_b200 import d2f, lopa
 
 dev = "cuda:0"
+
+
+def _checked_violations():
+    """Violations counted by a -DLOPA_CHECKED build (LOPA_LIB_VARIANT=checked), else 0."""
+    import ctypes
+    out = (ctypes.c_uint32 * 3)()
+    st = lopa.lib().lopa_debug_check_read(ctypes.cast(out, ctypes.c_void_p))
+    if st == 0 and out[0]:
+        raise AssertionError(f"checked build: {out[0]} violations, first site {out[1]}, sites {out[2]:#x}")
+    return st == 0
+
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 t0 = time.time()
@@ -73,5 +84,8 @@ while time.time() - t0 < budget:
                (h.forwards, h.windows, h.winners, h.branch_counts, h.commits), ("D2F", B, L_, k, mw, seed)
         assert torch.equal(g.tokens, h.tokens)
         n_d2f += 1
-print(f"stress_r02: {n_bp} BP decodes ({n_checked} steps oracle-checked), {n_d2f} device D2F "
+    if (n_bp + n_d2f) % 200 == 0:
+        _checked_violations()
+checked = _checked_violations()
+print(("checked build, 0 violations; " if checked else "") + f"stress_r02: {n_bp} BP decodes ({n_checked} steps oracle-checked), {n_d2f} device D2F "
       f"decodes, {time.time() - t0:.0f} s, no failure")
