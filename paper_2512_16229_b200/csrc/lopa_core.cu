@@ -622,7 +622,12 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
     }
     return;
   }
+#ifdef LOPA_K2_DEFER_STORES
+  // experiment: the scores / winner reach global memory only after the decisions
+  cta_scores<NT, S>(T, P, nb, W, warp, lane, nullptr);
+#else
   cta_scores<NT, S>(T, P, nb, W, warp, lane, P.scores);
+#endif
   __syncthreads();
   if (tid == 0) TLC(22);
   if (tid == 0) CHSET(T.stamp, 7);
@@ -659,7 +664,11 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
       n_mb0 += __popc(__ballot_sync(0xffffffffu, r.msk[h]));
     }
     if (lane == 0) {
+#ifdef LOPA_K2_DEFER_STORES
+      T.best = w;
+#else
       *P.winner = w;
+#endif
       T.n = any ? min(P.k, n_mb0) : -1;
     }
   }
@@ -709,6 +718,10 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
     }
   }
   if (tid == 0) *P.n_next = nl + 1;
+#ifdef LOPA_K2_DEFER_STORES
+  if (tid == 0) *P.winner = T.best;
+  for (int j = tid; j < P.cap; j += kPos) P.scores[j] = T.scores[j];
+#endif
   if (tid == 0) CHSET(T.stamp, 10);
   TL(13);
 }
@@ -1634,76 +1647,74 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   if (MODE != MODE_DECIDE) {
     // Fold every masked row as soon as its n_grp partials of THIS launch have landed (each
     // 64-bit half self-validating, store_partial), while K1 still streams: no grid-wide wait.
-    for (int rc = tid; rc < n_masked; rc += kTailThreads) {
-      const int row = rows[rc];
-      const float4* q = P.gpart + row;
-      FoldAcc f;
-      if (n_grp <= 16) {
-        // poll the row's pending slots (all loads in flight at once); a slot whose two halves
-        // both carry this launch's epoch is decoded into this thread's scratch column
-        uint32_t pend = (1u << n_grp) - 1u;
-        for (uint32_t spin = 0;; ++spin) {
+    // poll one masked row's n_grp partials and fold them (conf, argmax -> global and T)
+    auto poll_fold_row = [&](const int row) {
+        const float4* q = P.gpart + row;
+        FoldAcc f;
+        if (n_grp <= 16) {
+          // poll the row's pending slots (all loads in flight at once); a slot whose two halves
+          // both carry this launch's epoch is decoded into this thread's scratch column
+          uint32_t pend = (1u << n_grp) - 1u;
+          for (uint32_t spin = 0;; ++spin) {
 #pragma unroll
-          for (int h = 0; h < 16; h += 8) {  // two batches of 8 loads in flight
-            uint64_t A[8], B[8];
+            for (int h = 0; h < 16; h += 8) {  // two batches of 8 loads in flight
+              uint64_t A[8], B[8];
 #pragma unroll
-            for (int p = 0; p < 8; ++p)
-              if ((pend >> (h + p)) & 1u) load_partial_raw(q + (size_t)(h + p) * P.n_cand, &A[p], &B[p]);
+              for (int p = 0; p < 8; ++p)
+                if ((pend >> (h + p)) & 1u) load_partial_raw(q + (size_t)(h + p) * P.n_cand, &A[p], &B[p]);
 #pragma unroll
-            for (int p = 0; p < 8; ++p)
-              if (((pend >> (h + p)) & 1u) && stamped(A[p], B[p], stamp)) {
-                pscr[(h + p) * kTailThreads + tid] = decode_partial(A[p], B[p]);
-                pend &= ~(1u << (h + p));
-              }
-          }
-          if (!pend) break;
-          if (spin >= kPollSpins) {
-            atomicOr(P.dev_status, kDevInternal);
-            LOPA_CHK(false, 6);
-            break;
-          }
-          __nanosleep(64);
-        }
-        float4 qr[16];
-#pragma unroll
-        for (int p = 0; p < 16; ++p)
-          qr[p] = (p < n_grp && !((pend >> p) & 1u))
-                      ? pscr[p * kTailThreads + tid]
-                      : make_float4(-INFINITY, 0.f, __uint_as_float(0xFFFFFFFFu), 0.f);
-        f = fold_tree16(n_grp, qr);
-      } else {
-        // > 16 groups (V > 2^18): poll each partial in turn, then the sequential fold re-reads
-        // them (already stamped, so the values are final)
-        for (int p = 0; p < n_grp; ++p) {
-          uint64_t A, B;
-          uint32_t spin = 0;
-          for (load_partial_raw(q + (size_t)p * P.n_cand, &A, &B); !stamped(A, B, stamp);
-               load_partial_raw(q + (size_t)p * P.n_cand, &A, &B)) {
-            if (++spin >= kPollSpins) {
+              for (int p = 0; p < 8; ++p)
+                if (((pend >> (h + p)) & 1u) && stamped(A[p], B[p], stamp)) {
+                  pscr[(h + p) * kTailThreads + tid] = decode_partial(A[p], B[p]);
+                  pend &= ~(1u << (h + p));
+                }
+            }
+            if (!pend) break;
+            if (spin >= kPollSpins) {
               atomicOr(P.dev_status, kDevInternal);
               LOPA_CHK(false, 6);
               break;
             }
             __nanosleep(64);
           }
+          float4 qr[16];
+#pragma unroll
+          for (int p = 0; p < 16; ++p)
+            qr[p] = (p < n_grp && !((pend >> p) & 1u))
+                        ? pscr[p * kTailThreads + tid]
+                        : make_float4(-INFINITY, 0.f, __uint_as_float(0xFFFFFFFFu), 0.f);
+          f = fold_tree16(n_grp, qr);
+        } else {
+          // > 16 groups (V > 2^18): poll each partial in turn, then the sequential fold re-reads
+          // them (already stamped, so the values are final)
+          for (int p = 0; p < n_grp; ++p) {
+            uint64_t A, B;
+            uint32_t spin = 0;
+            for (load_partial_raw(q + (size_t)p * P.n_cand, &A, &B); !stamped(A, B, stamp);
+                 load_partial_raw(q + (size_t)p * P.n_cand, &A, &B)) {
+              if (++spin >= kPollSpins) {
+                atomicOr(P.dev_status, kDevInternal);
+                LOPA_CHK(false, 6);
+                break;
+              }
+              __nanosleep(64);
+            }
+          }
+          f = fold_seq(n_grp, [&](int p) {
+            uint64_t A, B;
+            load_partial_raw(q + (size_t)p * P.n_cand, &A, &B);
+            return decode_partial(A, B);
+          });
         }
-        f = fold_seq(n_grp, [&](int p) {
-          uint64_t A, B;
-          load_partial_raw(q + (size_t)p * P.n_cand, &A, &B);
-          return decode_partial(A, B);
-        });
-      }
-      LOPA_CHK(row < P.n_cand, 7);
-#ifdef LOPA_TIMELINE
-      if (rc == 0) tl_clk_dep(17, f.S);
-#endif
-      const float c = __fdiv_rn(1.0f, f.S);
-      P.conf[row] = c;
-      P.argmax[row] = (int32_t)f.a;
-      if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
-      T.conf[row] = c;
-      T.amax[row] = (int32_t)f.a;
-    }
+        LOPA_CHK(row < P.n_cand, 7);
+        const float c = __fdiv_rn(1.0f, f.S);
+        P.conf[row] = c;
+        P.argmax[row] = (int32_t)f.a;
+        if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
+        T.conf[row] = c;
+        T.amax[row] = (int32_t)f.a;
+    };
+    for (int rc = tid; rc < n_masked; rc += kTailThreads) poll_fold_row(rows[rc]);
   } else {
     grid_dep_wait();  // MODE_DECIDE: conf / argmax written by the previous kernel
     for (int rc = tid; rc < n_masked; rc += kTailThreads) {
