@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblopa.so")
 SOURCES = ["lopa_core.cu", "lopa_syn.cu", "lopa_bp.cu", "lopa_lmhead.cu", "lopa_d2f.cu", "lopa_graph.cu"]
-HEADERS = ["lopa_ptx.cuh", "lopa_decide.cuh", "lopa_internal.h"]
+HEADERS = ["lopa_ptx.cuh", "lopa_decide.cuh", "lopa_internal.h", "lopa_k1_ldg.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
