@@ -88,3 +88,43 @@ def test_d2f_device_matches_host_pipeline_k15(mods):
     assert g.forwards == h.forwards and g.windows == h.windows and g.winners == h.winners
     assert g.branch_counts == h.branch_counts and g.commits == h.commits
     assert torch.equal(g.tokens, h.tokens)
+
+
+@pytest.mark.parametrize("seed,V,L,B,k,tau_add,mw,extras,metric,param", [
+    (20, 64, 32, 32, 0, 0.1, 256, 1, 0, 0.0),      # k = 0: the Eq. 1 baseline through the pipeline
+    (21, 64, 256, 256, 3, 0.1, 256, 1, 0, 0.0),    # one block of 256 = the largest window
+    (22, 64, 64, 8, 5, 0.1, 256, 1, 1, 3.0),       # Eq. 2 sliding-window minimum
+    (23, 64, 64, 8, 5, 0.1, 256, 1, 2, 0.5),       # Eq. 2 least-confident half
+    (24, 1000, 48, 16, 31, 0.1, 48, 0, 0, 0.0),    # k = 31 with windows capped at 48
+])
+def test_d2f_device_loop_edges(mods, seed, V, L, B, k, tau_add, mw, extras, metric, param):
+    """Edge configurations of the device scheduler against the host pipeline (itself checked
+    against the oracle), run as one self-terminating graph launch."""
+    d2f, lopa = mods
+    cfg = d2f.BlockConfig(B, tau_add, 0.95, 0.9, mw)
+    h = d2f.decode_d2f(lambda b, t, m: lopa.syn_generate(seed, b, V, t, m, extras=extras), L, k, cfg, V, DEV,
+                       metric=metric, metric_param=param)
+    loop = d2f.D2FDeviceLoop(L, k, cfg, V, DEV, seed, extras=extras, metric=metric, metric_param=param)
+    wg = loop.capture_while()
+    loop.reset()
+    loop.launch_while()
+    torch.cuda.synchronize()
+    g = loop.trace()
+    assert wg.iterations() == h.forwards == g.forwards
+    assert g.windows == h.windows and g.winners == h.winners and g.branch_counts == h.branch_counts
+    assert g.commits == h.commits and torch.equal(g.tokens, h.tokens)
+    wg.close()
+
+
+def test_d2f_device_loop_matches_oracle_metric(mods):
+    """An Eq. 2 variant through the device scheduler against the oracle's D2F loop directly."""
+    d2f, lopa = mods
+    V, L, B, k = 64, 48, 8, 4
+    cfg = d2f.BlockConfig(B, 0.25, 0.95, 0.9, 256)
+    r = D.decode_d2f(lambda b, t, m: syngen.gen_logits(30, b, V, t, m, extras=1), L, B, k, 0.25,
+                     0.95, 0.9, max_window=256)
+    loop = d2f.D2FDeviceLoop(L, k, cfg, V, DEV, 30, extras=1)
+    loop.reset()
+    loop.run(r.forwards + 2)
+    torch.cuda.synchronize()
+    _assert_same(loop.trace(), r)
