@@ -414,9 +414,29 @@ def run_lopa(args):
     L = lopa.lib()
 
     bp = None
+    p2p_note = None
     if use_bp:
-        # LOPA_BP_P2P=1: the record exchange over peer memory (lopa_bp_step_p2p) instead of NCCL
-        bp = lopa.BranchParallel(st, rank, world, p2p=os.environ.get("LOPA_BP_P2P") == "1")
+        # the record exchange over peer memory (lopa_bp_step_p2p: K2 stores its record into every
+        # peer over NVLink and finishes the step itself) by default at N > 1; LOPA_BP_P2P=0 forces
+        # the NCCL all-gather (the default at N = 1, where there is no peer).  If the peer-memory
+        # setup or a first exchange fails, the run falls back to NCCL and says so in the line.
+        want_p2p = os.environ.get("LOPA_BP_P2P", "1" if world > 1 else "0") == "1"
+        ok = False
+        if want_p2p:
+            try:
+                bp = lopa.BranchParallel(st, rank, world, p2p=True)
+                ok = True
+            except Exception as e:  # noqa: BLE001 - reported in the bench line
+                p2p_note = f"peer-memory setup failed ({type(e).__name__}: {e}); NCCL all-gather used"
+        if dist is not None and want_p2p:
+            flag = torch.tensor([1 if ok else 0], device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if ok and int(flag.item()) == 0:
+                bp.close()
+                ok = False
+                p2p_note = p2p_note or "peer-memory setup failed on another rank; NCCL all-gather used"
+        if not ok:
+            bp = lopa.BranchParallel(st, rank, world, p2p=False)
 
     # prebuilt argument structs (one per rotating buffer): the timed loop only launches
     if bp is None:
@@ -450,6 +470,12 @@ def run_lopa(args):
     for i in range(args.warmup):
         launch(i)
     torch.cuda.synchronize()
+    if bp is not None and bp.p2p:
+        bad = torch.tensor([1 if int(st.out.status.item()) & 4 else 0], device=dev)  # PEER_TIMEOUT
+        if dist is not None:
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if int(bad.item()):
+            raise RuntimeError("peer-memory exchange timed out during the warm-up; rerun with LOPA_BP_P2P=0")
 
     # timed region (headline): K steps back to back, events only at the ends (so the PDL overlap
     # between a step's kernels and the next step's is not broken by interleaved event records)
@@ -753,6 +779,9 @@ def run_lopa(args):
                        "branches": int(nb.item()), "masked_rows": rows_total,
                        "masked_rows_this_rank": rows_local,
                        "parallelism": (f"bp{world}" + ("-p2p" if bp.p2p else "")) if bp is not None else "single",
+                       "bp_exchange": (None if bp is None else
+                                       ("peer memory, fused into K2 (lopa_bp_step_p2p)" if bp.p2p else "NCCL all-gather")
+                                       + ("" if p2p_note is None else f" [{p2p_note}]")),
                        "l2": f"rotating {n_buf} logits buffers ({n_buf * full.numel() * 2 / 1e6:.0f} MB >= 4x L2)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -768,7 +797,7 @@ def run_lopa(args):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "_fallback" not in pk else "fallback"},
             "logits_gbs_step": alg_bytes / (el_ms / K / 1000.0) / 1e9,
             "clocks": clk.summary(),
-            "gpu_launches": K * (2 if bp is None else 3),
+            "gpu_launches": K * (2 if bp is None or bp.p2p else 3),
         }
         if e2e is not None:
             line["e2e"] = e2e

@@ -133,6 +133,7 @@ extern "C" void lopa_bp_destroy(lopa_bp_t* bp) {
 // ---- peer-memory exchange ---------------------------------------------------------------------
 static_assert(sizeof(cudaIpcMemHandle_t) == LOPA_BP_IPC_HANDLE_BYTES, "IPC handle size");
 
+#ifdef LOPA_BP_P2P_3K
 namespace {
 // One CTA: copy this rank's record (rb bytes, 16-byte units) into slot `rank` of the current
 // parity of every peer, then, after a system-scope fence, raise this rank's flag to `epoch`
@@ -159,6 +160,7 @@ __global__ void bp_publish_kernel(uint8_t* const* peer_base, int world, int rank
   }
 }
 }  // namespace
+#endif
 
 extern "C" int lopa_bp_p2p_alloc(lopa_bp_t* bp, int32_t window, int32_t b_loc, size_t payload_bytes,
                                  void* handle_out) {
@@ -213,9 +215,15 @@ extern "C" int lopa_bp_step_p2p(lopa_bp_t* bp, const lopa_step_args_t* args, int
   const size_t rb = bp->p2p_rb;
   uint8_t* records = bp->p2p_base + (size_t)parity * bp->world * rb;
   uint8_t* mine = records + rb * bp->rank;
+  const size_t flags_off = 2 * (size_t)bp->world * rb;
+#ifndef LOPA_BP_P2P_3K
+  // one fused kernel after K1: local half, NVLink stores + flags, wait, global half
+  return lopa::launch_bp_fused(args, b_loc, mine, (uint8_t* const*)bp->d_peer_base, bp->world,
+                               bp->rank, rb, flags_off, parity, epoch, s);
+#else
+  // round-1 form: K2 (local half), a publish kernel, the finishing kernel
   int st = lopa::launch_bp_local(args, bp->rank * b_loc, b_loc, mine, s);
   if (st != LOPA_OK) return st;
-  const size_t flags_off = 2 * (size_t)bp->world * rb;
   {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(1);
@@ -232,6 +240,7 @@ extern "C" int lopa_bp_step_p2p(lopa_bp_t* bp, const lopa_step_args_t* args, int
   }
   return lopa::launch_bp_finish(args, b_loc, bp->world, records, s,
                                 reinterpret_cast<const uint32_t*>(bp->p2p_base + flags_off), epoch);
+#endif
 }
 
 // ---- Commit-Winner-Cache over peer memory ---------------------------------------------------------

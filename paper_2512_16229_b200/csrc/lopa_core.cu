@@ -150,7 +150,10 @@ static_assert(kConsumerWGs % kSegPerItem == 0, "warpgroups cover the segments of
 // tell consecutive phases apart), so each stage belongs to exactly one consumer phase.
 static_assert(kStages % kWgStride == 0, "stages must divide evenly among consumer phases");
 
-enum Mode : int { MODE_CONF = 0, MODE_STEP = 1, MODE_BP_LOCAL = 2, MODE_DECIDE = 3 };
+enum Mode : int { MODE_CONF = 0, MODE_STEP = 1, MODE_BP_LOCAL = 2, MODE_DECIDE = 3, MODE_BP_FUSED = 4 };
+// MODE_BP_FUSED: MODE_BP_LOCAL, then the peer-memory exchange and the global select / anchor /
+// spawn in the same kernel (lopa_bp_step_p2p: K2 stores its record into every peer over NVLink,
+// raises its epoch flag there, waits for every peer's, and finishes the step).
 // MODE_DECIDE: conf / argmax already in P.conf / P.argmax (the fused LM-head path); K2 only decides.
 
 struct Params {
@@ -165,6 +168,11 @@ struct Params {
   int32_t cap;                 // branch capacity of the logits / conf tables
   int32_t table_rows;          // rows of the replicated branch tables (max_branches; n_rows / 1 for a1 alone)
   int32_t k1_alone;            // K1 launched without a consumer (lopa_debug_reduce_only)
+  // MODE_BP_FUSED: the peer-memory exchange (lopa_bp_step_p2p)
+  uint8_t* const* peer_base;   // device array: every rank's mapped exchange buffer
+  int32_t bp_world, bp_rank, bp_b_loc, bp_parity;
+  uint32_t bp_epoch;
+  int64_t bp_rb, bp_flags_off;
   const int32_t* window_dev;   // nullable: the window read on the device (lopa_d2f_* loop);
                                // n_cand = cap * window then (see with_device_window)
   float* conf;
@@ -1139,6 +1147,12 @@ __device__ __forceinline__ FoldAcc fold_row_smem(const float4* q, int n_grp, int
   return fold_seq(n_grp, [&](int p) { return q[p * stride]; });
 }
 
+__device__ bool bp_wait_flags(const Params& P, const uint32_t* flags, int world, uint32_t epoch,
+                              int lane);
+template <int S>
+__device__ void bp_finish_warp(const Params& P, const uint8_t* records, int world, int b_loc,
+                               int n_scores, uint64_t* keys, int lane);
+
 template <int MODE, int S>
 __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params P_arg) {
   // launched by K1's launch_dependents, i.e. after K1's own wait: a device window is final
@@ -1392,7 +1406,37 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   __syncthreads();
 #endif
   if (MODE == MODE_STEP || MODE == MODE_DECIDE) cta_tail_step<kTailThreads, S>(P, T, tid, nb);
-  if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads, S>(P, T, tid, nb);
+  if (MODE == MODE_BP_LOCAL || MODE == MODE_BP_FUSED) cta_tail_bp_local<kTailThreads, S>(P, T, tid, nb);
+  if (MODE == MODE_BP_FUSED) {
+    // the exchange in the same kernel: this rank's record (its slot of this epoch's parity) is
+    // stored into the same slot of every peer over NVLink, then this rank's epoch flag is raised
+    // in every peer (system-scope release after a system fence; the CTA barrier orders every
+    // thread's stores before it), then warp 0 waits for every rank's flag and finishes the step
+    __syncthreads();
+    const size_t rb = (size_t)P.bp_rb;
+    const size_t slot = ((size_t)P.bp_parity * P.bp_world + P.bp_rank) * rb;
+    const uint4* src = reinterpret_cast<const uint4*>(P.record);
+    for (int q = 0; q < P.bp_world; ++q) {
+      if (q == P.bp_rank) continue;
+      uint4* dst = reinterpret_cast<uint4*>(P.peer_base[q] + slot);
+      for (size_t e = tid; e < rb / 16; e += kTailThreads) dst[e] = src[e];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      for (int q = 0; q < P.bp_world; ++q) {
+        uint32_t* f = reinterpret_cast<uint32_t*>(P.peer_base[q] + P.bp_flags_off) + P.bp_rank;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(P.bp_epoch) : "memory");
+      }
+    }
+    if (warp == 0) {
+      uint8_t* own = P.peer_base[P.bp_rank];
+      const uint32_t* flags = reinterpret_cast<const uint32_t*>(own + P.bp_flags_off);
+      if (bp_wait_flags(P, flags, P.bp_world, P.bp_epoch, lane))
+        bp_finish_warp<S>(P, own + (size_t)P.bp_parity * P.bp_world * rb, P.bp_world, P.bp_b_loc,
+                          P.table_rows, T.keys, lane);
+    }
+  }
   if (tid == 0) {
     TL(5);
     TLC(20);
@@ -1538,41 +1582,42 @@ __global__ void verify_ex_kernel(const float* conf, const uint8_t* mask, const i
   if (lane == 0) *winner = w;
 }
 
-// Global half of a BP step: one warp; lane r reads record r's header.
-template <int S>
-__global__ void bp_finish_kernel(const Params P, const uint8_t* records, int world, int b_loc,
-                                 int n_scores, const uint32_t* flags, uint32_t epoch) {
-  __shared__ uint64_t keys[32 * S];
-  const int lane = threadIdx.x;
-  grid_dep_wait();  // PDL (peer-memory path): the publisher before us has been issued
-  if (flags != nullptr) {
-    // peer-memory exchange (lopa_bp_step_p2p): wait until every rank's record of this epoch
-    // has landed (acquire at system scope pairs with the publisher's release); a rank that
-    // never arrives (bounded spin) is reported as LOPA_DEV_PEER_TIMEOUT instead of hanging
-    if (lane < world) {
-      uint32_t v = 0;
-      for (uint32_t spin = 0; spin < (1u << 26); ++spin) {
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + lane) : "memory");
-        if (v >= epoch) break;
-        __nanosleep(64);
-      }
-      if (v < epoch) atomicOr(P.dev_status, kDevPeerTimeout);
-    }
-    // a rank that never arrived: decide nothing from stale or partial records -- the step ends
-    // with no branch (n_next = 0) and the tables untouched; the caller must check dev_status
-    // after every peer-memory step (liblopa.h, lopa_bp_step_p2p)
-    bool late = false;
-    if (lane < world) {
-      uint32_t v;
+// Peer-memory exchange: wait (one warp; lane r polls rank r's flag, acquire at system scope,
+// bounded) until every rank's record of this epoch has landed.  A rank that never arrives is
+// reported as LOPA_DEV_PEER_TIMEOUT and the step decides nothing (n_next = 0, tables untouched:
+// the caller must check dev_status after every peer-memory step).  Returns false then.
+__device__ bool bp_wait_flags(const Params& P, const uint32_t* flags, int world, uint32_t epoch,
+                              int lane) {
+  if (lane < world) {
+    uint32_t v = 0;
+    // bounded (~0.1-0.2 s): a healthy exchange lands within microseconds
+    for (uint32_t spin = 0; spin < (1u << 21); ++spin) {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + lane) : "memory");
-      late = v < epoch;
+      if (v >= epoch) break;
+      __nanosleep(64);
     }
-    if (__any_sync(0xffffffffu, late)) {
-      if (lane == 0) *P.n_next = 0;
-      return;
-    }
-    __syncwarp();
+    if (v < epoch) atomicOr(P.dev_status, kDevPeerTimeout);
   }
+  bool late = false;
+  if (lane < world) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + lane) : "memory");
+    late = v < epoch;
+  }
+  if (__any_sync(0xffffffffu, late)) {
+    if (lane == 0) *P.n_next = 0;
+    return false;
+  }
+  __syncwarp();
+  return true;
+}
+
+// Global half of a BP step on one warp over the `world` records (lane r reads record r's
+// header): the global select, the scores of every branch, the anchor on the owner's row and the
+// spawn.  keys: 32 S entries of shared scratch.
+template <int S>
+__device__ void bp_finish_warp(const Params& P, const uint8_t* records, int world, int b_loc,
+                               int n_scores, uint64_t* keys, int lane) {
   const size_t rb = record_bytes(b_loc);
   float bs = -INFINITY;
   int bid = 0x7FFFFFFF;
@@ -1640,6 +1685,18 @@ __global__ void bp_finish_kernel(const Params P, const uint8_t* records, int wor
   warp_spawn<S>(r, W, P.k, keys, P.next_tokens, P.next_mask, P.lookahead, P.n_next, lane);
 }
 
+// Global half of a BP step as its own kernel (NCCL all-gather path; flags: the round-1
+// three-kernel peer-memory path, LOPA_BP_P2P_3K).
+template <int S>
+__global__ void bp_finish_kernel(const Params P, const uint8_t* records, int world, int b_loc,
+                                 int n_scores, const uint32_t* flags, uint32_t epoch) {
+  __shared__ uint64_t keys[32 * S];
+  const int lane = threadIdx.x;
+  grid_dep_wait();  // PDL (peer-memory path): the publisher before us has been issued
+  if (flags != nullptr && !bp_wait_flags(P, flags, world, epoch, lane)) return;
+  bp_finish_warp<S>(P, records, world, b_loc, n_scores, keys, lane);
+}
+
 // ------------------------------------------------------------------ host helpers
 static std::mutex g_mu;
 static int g_sms[64];
@@ -1664,6 +1721,8 @@ static TailKernel tail_kernel_for(int mode, int window) {
     return S == 1 ? lopa_tail_kernel<MODE_STEP, 1> : S == 2 ? lopa_tail_kernel<MODE_STEP, 2> : lopa_tail_kernel<MODE_STEP, 8>;
   if (mode == MODE_DECIDE)
     return S == 1 ? lopa_tail_kernel<MODE_DECIDE, 1> : S == 2 ? lopa_tail_kernel<MODE_DECIDE, 2> : lopa_tail_kernel<MODE_DECIDE, 8>;
+  if (mode == MODE_BP_FUSED)
+    return S == 1 ? lopa_tail_kernel<MODE_BP_FUSED, 1> : S == 2 ? lopa_tail_kernel<MODE_BP_FUSED, 2> : lopa_tail_kernel<MODE_BP_FUSED, 8>;
   return S == 1 ? lopa_tail_kernel<MODE_BP_LOCAL, 1> : S == 2 ? lopa_tail_kernel<MODE_BP_LOCAL, 2> : lopa_tail_kernel<MODE_BP_LOCAL, 8>;
 }
 
@@ -1687,7 +1746,7 @@ static int ensure_kernel_attrs(int device) {
     e = cudaFuncSetAttribute(lopa_reduce_ldg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kLSmemBytes);
 #endif
-  for (int mode : {(int)MODE_STEP, (int)MODE_BP_LOCAL, (int)MODE_DECIDE})
+  for (int mode : {(int)MODE_STEP, (int)MODE_BP_LOCAL, (int)MODE_DECIDE, (int)MODE_BP_FUSED})
     for (int w : {32, 64, 256})
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(tail_kernel_for(mode, w), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1909,6 +1968,40 @@ int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_lo
   P.n_cand = b_loc * a->window;
   P.row_mask = a->branch_mask + (size_t)branch_base * a->window;
   P.record = static_cast<uint8_t*>(record);
+  return launch_reduce(P, dev, s);
+}
+
+// lopa_bp_step_p2p in two kernels: K1 + K2 in MODE_BP_FUSED (local half, the peer-memory
+// exchange and the global half).  record = this rank's slot of this epoch's parity.
+int launch_bp_fused(const lopa_step_args_t* a, int32_t b_loc, void* record, uint8_t* const* peer_base,
+                    int32_t world, int32_t rank, size_t rb, size_t flags_off, int32_t parity,
+                    uint32_t epoch, cudaStream_t s) {
+  int st = validate_step_args(a, true, true);
+  if (st != LOPA_OK) return st;
+  if (!record || !peer_base || b_loc < 1 || world < 1 || world > 32 || rank < 0 || rank >= world)
+    return LOPA_ERR_INVALID_ARG;
+  if (b_loc > LOPA_MAX_BRANCHES || (int64_t)b_loc * a->window > LOPA_MAX_ROWS)
+    return LOPA_ERR_UNSUPPORTED;
+  Workspace ws;
+  if (!carve_workspace(a->workspace, a->workspace_bytes, b_loc * a->window, a->vocab, &ws))
+    return LOPA_ERR_INVALID_ARG;
+  int dev;
+  if (!bind_device(s, a->logits, &dev)) return LOPA_ERR_CUDA;
+  Params P = base_params(a, ws);
+  P.mode = MODE_BP_FUSED;
+  P.branch_base = rank * b_loc;
+  P.cap = b_loc;
+  P.n_cand = b_loc * a->window;
+  P.row_mask = a->branch_mask + (size_t)P.branch_base * a->window;
+  P.record = static_cast<uint8_t*>(record);
+  P.peer_base = peer_base;
+  P.bp_world = world;
+  P.bp_rank = rank;
+  P.bp_b_loc = b_loc;
+  P.bp_parity = parity;
+  P.bp_epoch = epoch;
+  P.bp_rb = (int64_t)rb;
+  P.bp_flags_off = (int64_t)flags_off;
   return launch_reduce(P, dev, s);
 }
 

@@ -55,6 +55,9 @@ int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, co
                      cudaStream_t s, const uint32_t* flags = nullptr, uint32_t epoch = 0);
 int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_loc, void* record,
                     cudaStream_t s);
+int launch_bp_fused(const lopa_step_args_t* a, int32_t b_loc, void* record, uint8_t* const* peer_base,
+                    int32_t world, int32_t rank, size_t rb, size_t flags_off, int32_t parity,
+                    uint32_t epoch, cudaStream_t s);
 int validate_step_args(const lopa_step_args_t* a, bool need_next, bool need_logits = true);
 int launch_step_decide(const lopa_step_args_t* a, cudaStream_t s);
 
