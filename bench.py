@@ -870,7 +870,8 @@ def run_loop(args):
     V, W, k, tau, seed, nblk = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["seed"], CFG["loop_blocks"]
     st = lopa.Stepper(V, W, k + 1, k, tau, dev)
     use_bp = world > 1 or os.environ.get("LOPA_BENCH_FORCE_BP") == "1"
-    drv = lopa.BranchParallel(st, rank, world, p2p=os.environ.get("LOPA_BP_P2P") == "1") if use_bp else _SingleGPU(st)
+    drv = (lopa.BranchParallel(st, rank, world, p2p=os.environ.get("LOPA_BP_P2P", "1" if world > 1 else "0") == "1")
+           if use_bp else _SingleGPU(st))
     _, lo, hi, _buf = drv.ranks()[0]
     stream = torch.cuda.current_stream(dev)
 
@@ -999,7 +1000,7 @@ def run_loop(args):
     # the recorded trajectory replayed as ONE static CUDA graph (the step count of every block from
     # the recording; no host read): the device time of the LoPA loop itself on resident logits
     graph_replay = None
-    if not getattr(drv, "p2p", False):
+    if True:  # both exchanges are graph safe (the peer-memory epoch lives on the device)
         def replay_all():
             for blk in range(nblk):
                 tok.zero_()
@@ -1050,7 +1051,7 @@ def run_loop(args):
     # the same decode with each block ONE device-terminated CUDA graph (conditional WHILE node;
     # no host read at all; the SYN-D2F forward of this rank's branches inside the loop)
     dev_loop = None
-    if not getattr(drv, "p2p", False):
+    if True:
         graphs = [(lopa.DecodeBlockGraphBP(drv, seed, blk) if use_bp else lopa.DecodeBlockGraph(st, seed, blk))
                   for blk in range(nblk)]
         t0_ = torch.zeros(W, dtype=torch.int32, device=dev)
@@ -1077,7 +1078,8 @@ def run_loop(args):
         dev_loop = {"us_per_step_incl_forward": dl_ms * 1000.0 / steps_per_pass,
                     "ms_per_pass": dl_ms, "forwards_per_block": fw_dl,
                     "note": "each block one device-terminated CUDA graph (lopa.DecodeBlockGraph"
-                            + ("BP, NCCL all-gather inside the graph" if use_bp else "") +
+                            + (("BP, peer-memory exchange fused into K2, epoch on the device" if getattr(drv, "p2p", False)
+                                else "BP, NCCL all-gather inside the graph") if use_bp else "") +
                             "): no host read; includes the SYN-D2F forward of this rank's branches"}
         for g_ in graphs:
             g_.graph.close()

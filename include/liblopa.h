@@ -387,8 +387,12 @@ int lopa_syn_generate(uint64_t seed, int32_t block, int32_t vocab, int64_t ld, i
  *     communicator.
  *   lopa_bp_p2p_open: all_handles = the world handles in rank order (gathered by the caller);
  *     maps every peer's buffers.
- *   lopa_bp_step_p2p: as lopa_bp_step (args, b_loc), on the P2P buffers.  A peer that never
- *     arrives within the bounded wait sets LOPA_DEV_PEER_TIMEOUT and ends the step with
+ *   lopa_bp_step_p2p: as lopa_bp_step (args, b_loc), on the P2P buffers: K1, then ONE kernel
+ *     that computes the local record, stores it into every peer over NVLink, raises this rank's
+ *     epoch flag there, waits for every rank's flag and runs the global select / anchor / spawn.
+ *     The epoch lives in device memory, so the step may be captured in CUDA graphs (the
+ *     Commit-Winner-Cache payload slots below stay host-driven).  A peer that never arrives
+ *     within the bounded wait sets LOPA_DEV_PEER_TIMEOUT and ends the step with
  *     n_branches_next = 0 (tables untouched): callers check dev_status after every step.
  * Errors: LOPA_ERR_INVALID_ARG (order of calls, sizes), LOPA_ERR_CUDA (allocation, IPC). */
 #define LOPA_BP_IPC_HANDLE_BYTES 64

@@ -217,7 +217,10 @@ extern "C" int lopa_bp_step_p2p(lopa_bp_t* bp, const lopa_step_args_t* args, int
   uint8_t* mine = records + rb * bp->rank;
   const size_t flags_off = 2 * (size_t)bp->world * rb;
 #ifndef LOPA_BP_P2P_3K
-  // one fused kernel after K1: local half, NVLink stores + flags, wait, global half
+  // one fused kernel after K1: local half, NVLink stores + flags, wait, global half.  The kernel
+  // keeps the exchange epoch on the device (graph safe); the host count above tracks it for
+  // the payload slots of the Commit-Winner-Cache (lopa_bp_payload_slots / _commit_winner_p2p),
+  // which therefore stay host-driven
   return lopa::launch_bp_fused(args, b_loc, mine, (uint8_t* const*)bp->d_peer_base, bp->world,
                                bp->rank, rb, flags_off, parity, epoch, s);
 #else

@@ -737,10 +737,11 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
 // Local half of a BP step with all threads of K2: local Eq. 2 scores, local best
 // (smallest local j with the largest score), and the exchange record.
 template <int NT, int S>
-__device__ void cta_tail_bp_local(const Params& P, TailSmem& T, int tid, int nb) {
+__device__ void cta_tail_bp_local(const Params& P, TailSmem& T, int tid, int nb,
+                                  uint8_t* record = nullptr) {
   const int warp = tid >> 5, lane = tid & 31;
   const int W = P.window;
-  RecordView rv = record_view(P.record, P.cap);
+  RecordView rv = record_view(record ? record : P.record, P.cap);
   cta_scores<NT, S>(T, P, nb, W, warp, lane, rv.scores);
   __syncthreads();
   if (warp == 0) {
@@ -1406,7 +1407,18 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   __syncthreads();
 #endif
   if (MODE == MODE_STEP || MODE == MODE_DECIDE) cta_tail_step<kTailThreads, S>(P, T, tid, nb);
-  if (MODE == MODE_BP_LOCAL || MODE == MODE_BP_FUSED) cta_tail_bp_local<kTailThreads, S>(P, T, tid, nb);
+  // MODE_BP_FUSED: this rank's exchange epoch lives in its own buffer (after the flags), so the
+  // step is CUDA-graph safe: e = counter + 1, records double-buffered by e's parity
+  uint32_t bp_e = 0;
+  uint8_t* bp_record = nullptr;
+  if (MODE == MODE_BP_FUSED) {
+    const uint32_t* ectr = reinterpret_cast<const uint32_t*>(P.peer_base[P.bp_rank] + P.bp_flags_off + 192);
+    bp_e = *ectr + 1u;
+    bp_record = P.peer_base[P.bp_rank] +
+                ((size_t)(bp_e & 1u) * P.bp_world + P.bp_rank) * (size_t)P.bp_rb;
+  }
+  if (MODE == MODE_BP_LOCAL) cta_tail_bp_local<kTailThreads, S>(P, T, tid, nb);
+  if (MODE == MODE_BP_FUSED) cta_tail_bp_local<kTailThreads, S>(P, T, tid, nb, bp_record);
   if (MODE == MODE_BP_FUSED) {
     // the exchange in the same kernel: this rank's record (its slot of this epoch's parity) is
     // stored into the same slot of every peer over NVLink, then this rank's epoch flag is raised
@@ -1414,8 +1426,9 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
     // thread's stores before it), then warp 0 waits for every rank's flag and finishes the step
     __syncthreads();
     const size_t rb = (size_t)P.bp_rb;
-    const size_t slot = ((size_t)P.bp_parity * P.bp_world + P.bp_rank) * rb;
-    const uint4* src = reinterpret_cast<const uint4*>(P.record);
+    const int parity = (int)(bp_e & 1u);
+    const size_t slot = ((size_t)parity * P.bp_world + P.bp_rank) * rb;
+    const uint4* src = reinterpret_cast<const uint4*>(bp_record);
     for (int q = 0; q < P.bp_world; ++q) {
       if (q == P.bp_rank) continue;
       uint4* dst = reinterpret_cast<uint4*>(P.peer_base[q] + slot);
@@ -1426,15 +1439,17 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
       __threadfence_system();
       for (int q = 0; q < P.bp_world; ++q) {
         uint32_t* f = reinterpret_cast<uint32_t*>(P.peer_base[q] + P.bp_flags_off) + P.bp_rank;
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(P.bp_epoch) : "memory");
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(bp_e) : "memory");
       }
     }
     if (warp == 0) {
       uint8_t* own = P.peer_base[P.bp_rank];
       const uint32_t* flags = reinterpret_cast<const uint32_t*>(own + P.bp_flags_off);
-      if (bp_wait_flags(P, flags, P.bp_world, P.bp_epoch, lane))
-        bp_finish_warp<S>(P, own + (size_t)P.bp_parity * P.bp_world * rb, P.bp_world, P.bp_b_loc,
+      if (bp_wait_flags(P, flags, P.bp_world, bp_e, lane))
+        bp_finish_warp<S>(P, own + (size_t)parity * P.bp_world * rb, P.bp_world, P.bp_b_loc,
                           P.table_rows, T.keys, lane);
+      if (lane == 0)  // the next step's epoch (read by the next K2 of this rank only)
+        *reinterpret_cast<uint32_t*>(own + P.bp_flags_off + 192) = bp_e;
     }
   }
   if (tid == 0) {

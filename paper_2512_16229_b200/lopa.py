@@ -570,12 +570,11 @@ class DecodeBlockGraphBP:
     present branches (syn_generate_dev on global branches [lo, hi), count read on the device),
     lopa_bp_step (local reduction and record, the NCCL all-gather, the replicated select /
     anchor / spawn) and the table copies, in one device-terminated graph per block (every rank
-    holds the same tables, so every rank's loop stops at the same iteration).  NCCL path only:
-    the peer-memory exchange keeps its epoch on the host and is not graph-capturable."""
+    holds the same tables, so every rank's loop stops at the same iteration).  Either exchange:
+    the NCCL all-gather is captured as a graph node, the peer-memory step keeps its epoch on the
+    device."""
 
     def __init__(self, bp: "BranchParallel", seed: int, block: int, extras: int = 0):
-        if bp.p2p:
-            raise LopaError("DecodeBlockGraphBP needs the NCCL exchange (p2p=False)")
         st = bp.s
         self.bp, self.s, self.seed, self.block, self.extras = bp, st, seed, block, extras
         d, W, mb = st.device, st.window, st.max_branches

@@ -87,3 +87,26 @@ def test_bp_decode_block_graph_nccl_single_rank(L):
         bp.close()
     assert fws == c["forwards_per_block"][:3]
     assert toks == c["tokens"][: 3 * c["W"]]
+
+
+def test_bp_decode_block_graph_p2p_single_rank(L):
+    """The same BP block graph with the fused peer-memory exchange (epoch on the device), each
+    block's graph launched twice: tokens and forwards equal the oracle's stored decode."""
+    import json
+    import os
+    c = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_decode_configs.json")))["dream_k15_256"]
+    st = L.Stepper(c["V"], c["W"], c["k"] + 1, c["k"], c["tau"], DEV)
+    bp = L.BranchParallel(st, 0, 1, p2p=True)
+    try:
+        for blk in range(3):
+            g = L.DecodeBlockGraphBP(bp, c["seed"], blk)
+            for _ in range(2):
+                t = g.run(torch.zeros(c["W"], dtype=torch.int32, device=DEV),
+                          torch.ones(c["W"], dtype=torch.uint8, device=DEV)).clone()
+                torch.cuda.synchronize()
+                assert int(st.out.status.item()) == 0
+                assert g.forwards() == c["forwards_per_block"][blk]
+                assert t.cpu().tolist() == c["tokens"][blk * c["W"]:(blk + 1) * c["W"]]
+            g.graph.close()
+    finally:
+        bp.close()
