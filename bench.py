@@ -1350,7 +1350,10 @@ def run_lmhead(args):
                    "l2": f"{NW} rotating weight copies ({NW * V * Kd * 2 / 1e9:.2f} GB >= L2)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "lopa_lmhead_kernel (tcgen05 LM head + Conf epilogue) + its fold",
+                     "kernel": (("lopa_lmhead_pair_kernel (CTA pairs, tcgen05.mma.cta_group::2 M=256, double-buffered TMEM accumulators)"
+                                 if rows > 128 and os.environ.get("LOPA_LMH_SINGLE") != "1" else
+                                 "lopa_lmhead_kernel (one CTA per SM, tcgen05.mma.cta_group::1)")
+                                + " + Conf epilogue + its fold"),
                      "kernel_ms_mean": kern_ms,
                      "kernel_timing": f"CUDA events around {K} back-to-back LMHead calls (GEMM+epilogue kernel and fold kernel)",
                      "alg_flops_per_launch": flops,

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -384,6 +385,296 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("griddepcontrol.launch_dependents;");
 }
 
+
+// ---- CTA-pair form (cta_group::2), rows 129..256 ---------------------------------------------
+// A cluster of two CTAs on one TPC computes each 256-row x N-column tile with one
+// tcgen05.mma.cta_group::2 (M = 256): CTA rank r holds rows [128 r, 128 r + 128) of the hidden
+// states and columns [N/2 r, N/2 (r + 1)) of the tile's weight rows in its shared memory, and
+// its TMEM receives its 128 rows x N columns.  So each CTA needs 256 TMEM columns per tile and
+// the accumulator is double-buffered (the MMA of tile t + 1 overlaps the epilogue of tile t),
+// and every MMA reads half of its operands from each SM's shared memory.  The leader (rank 0)
+// issues the MMAs; both CTAs' TMA loads complete on the leader's stage barriers; the commits
+// multicast to both CTAs; both epilogues release an accumulator on the leader's barrier.
+namespace pair {
+#ifndef LOPA_LMH2_STAGES
+#define LOPA_LMH2_STAGES 6
+#endif
+constexpr int kStages = LOPA_LMH2_STAGES;
+constexpr int kABytes = 128 * kBK * 2;   // 16 KB: this CTA's 128 rows
+constexpr int kBBytes = 128 * kBK * 2;   // 16 KB: this CTA's <= 128 weight rows
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kEpiWarps = 16;            // 4 lane quarters x 4 column groups
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kTmemCols = 512;
+constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 /*align*/ + 256 +
+                              3 * 128 * 16 /*column-group exchange*/;
+constexpr uint32_t kWaitLimit = 1u << 24;  // bounded waits: a lost arrival traps instead of hanging
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(saddr), "r"(rank));
+  return d;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void wait_bounded(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  for (uint32_t n = 0;; ++n) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(addr), "r"(parity), "r"(1000u) : "memory");
+    if (ok) return;
+    if (n == kWaitLimit) asm volatile("trap;");
+  }
+}
+// 2-D tile load into this CTA's shared memory, completing on the leader's barrier (cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint32_t bar_cluster, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on `bar` (same offset) in both CTAs of the pair once the issued MMAs completed
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+__device__ __forceinline__ void arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+// Tile t of a pair's nu units: ceil(nu / 16) tiles of near-equal width (multiples of 16 columns,
+// <= 256), so no tile is a narrow remainder whose hidden-state reloads would not hide under MMA.
+// The pair MMA needs N % 32 == 0 (16 weight rows per CTA; measured: N = 16·odd gives wrong
+// columns), so an odd-unit tile is computed 16 columns wider (Nm) and the epilogue ignores them.
+__device__ __forceinline__ void tile_cols_pair(int u0, int nu, int nt, int t, int* v0, int* N, int* Nm) {
+  const int a = (t * nu) / nt, e = ((t + 1) * nu) / nt;
+  *v0 = (u0 + a) * 16;
+  *N = (e - a) * 16;
+  *Nm = (*N + 31) & ~31;
+}
+
+// maps: A (box 128 rows); B boxes of 128, 64, 32 and 16 rows (Nm/2 rows = sum of set bits)
+struct BMaps {
+  CUtensorMap b[4];
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    lopa_lmhead_pair_kernel(const __grid_constant__ CUtensorMap map_a,
+                            const __grid_constant__ BMaps maps_b, const Args A) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;   // [2]
+  uint64_t* tempty = tfull + 2;        // [2] (the leader's are used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float4* xch = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 256);  // [3][128]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const int P = (int)gridDim.x / 2, p = (int)blockIdx.x / 2;
+  int u0, u1;
+  cta_range(p, P, A.n_units, &u0, &u1);
+  const int nu = u1 - u0;
+  const int n_tiles = (nu + 15) / 16;
+  const int nk = A.K / kBK;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer (both CTAs): this CTA's rows of A and half of the tile's weight rows
+      const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
+      uint32_t it = 0;
+      for (int t = 0; t < n_tiles; ++t) {
+        int v0, N, Nm;
+        tile_cols_pair(u0, nu, n_tiles, t, &v0, &N, &Nm);
+        const int nh = Nm / 2;  // weight rows per CTA (multiple of 16)
+        const int vb = v0 + (int)rank * nh;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = (int)(it % kStages);
+          if (it >= (uint32_t)kStages) wait_bounded(&empty[s], ((it / kStages) - 1) & 1);
+          uint8_t* sa = smem + (size_t)s * kStageBytes;
+          uint8_t* sb = sa + kABytes;
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * kABytes + Nm * kBK * 2));
+          const uint32_t bar = map_to_rank(smem_u32(&full[s]), 0);
+          tma_load_2d_pair(sa, &map_a, kb * kBK, (int)rank * 128, bar, pol_a);
+          int r = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int box = 128 >> i;
+            if (nh & box) {
+              tma_load_2d_pair(sb + r * kBK * 2, &maps_b.b[i], kb * kBK, vb + r, bar, pol_b);
+              r += box;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // ---- MMA issuer (leader only): M = 256 across the pair, N = the tile's columns
+      uint32_t it = 0;
+      for (int t = 0; t < n_tiles; ++t) {
+        int v0_unused, N, Nm;
+        tile_cols_pair(u0, nu, n_tiles, t, &v0_unused, &N, &Nm);
+        const int a = t & 1;
+        if (t >= 2) wait_bounded(&tempty[a], ((t >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t idesc = idesc_bf16(256, Nm);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = (int)(it % kStages);
+          wait_bounded(&full[s], (it / kStages) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint8_t* sa = smem + (size_t)s * kStageBytes;
+            const uint8_t* sb = sa + kABytes;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              mma_bf16_pair(tmem + (uint32_t)(a * 256), smem_desc_sw128(sa + kk * 32),
+                            smem_desc_sw128(sb + kk * 32), idesc, (kb | kk) != 0 ? 1u : 0u);
+            mma_commit_pair(&empty[s]);  // frees the stage in both CTAs
+          }
+          __syncwarp();
+        }
+        if (lane == 0) mma_commit_pair(&tfull[a]);  // accumulator complete in both CTAs
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---- epilogue: 16 warps; warp w reads TMEM lanes 32 (w % 4) .. +31 (hardware rule);
+    // column group g = (w - 2) >> 2 takes the 32-column chunks g, g + 4 of every tile.
+    const int ew = warp - 2;
+    const int g = ew >> 2;
+    const int q = warp & 3;
+    const int lrow = q * 32 + lane;                 // this CTA's row (TMEM lane)
+    const uint32_t tempty_leader = map_to_rank(smem_u32(&tempty[0]), 0);
+    float m = -INFINITY, ssum = 0.f;
+    int am = 0x7FFFFFFF;
+    for (int t = 0; t < n_tiles; ++t) {
+      int v0, N, Nm;
+      tile_cols_pair(u0, nu, n_tiles, t, &v0, &N, &Nm);
+      const int a = t & 1;
+      wait_bounded(&tfull[a], (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256);
+      for (int c0 = 32 * g; c0 < N; c0 += 128) {
+        float v[32];
+        tmem_ld32(base + (uint32_t)c0, v);
+        const int nv = min(min(32, N - c0), A.V - (v0 + c0));  // past the tile or V: not logits
+        if (nv < 32) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = i < nv ? v[i] : -INFINITY;
+        }
+        float cm = v[0];
+#pragma unroll
+        for (int i = 1; i < 32; ++i) cm = fmax_nan(cm, v[i]);
+        if (cm == -INFINITY) continue;
+        if (cm > m) {
+          int ci = 31;
+#pragma unroll
+          for (int i = 31; i >= 0; --i) ci = v[i] == cm ? i : ci;
+          ssum = (m == -INFINITY) ? 0.f : ssum * ex2((m - cm) * kLog2e);
+          m = cm;
+          am = v0 + c0 + ci;
+        } else if (cm != cm) {
+          m = cm;
+        }
+        float2 acc = make_float2(0.f, 0.f);
+        const float2 nm = make_float2(-m, -m), l2 = make_float2(kLog2e, kLog2e);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 d = __fmul2_rn(__fadd2_rn(make_float2(v[2 * i], v[2 * i + 1]), nm), l2);
+          acc = __fadd2_rn(acc, make_float2(ex2(d.x), ex2(d.y)));
+        }
+        ssum += acc.x + acc.y;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_cluster(tempty_leader + (uint32_t)(a * 8));
+    }
+    // combine the four column groups of each row in fixed order 0, 1, 2, 3
+    if (g > 0) xch[(g - 1) * 128 + lrow] = make_float4(m, ssum, __int_as_float(am), 0.f);
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpiWarps) : "memory");
+    const int row = (int)rank * 128 + lrow;
+    if (g == 0 && row < A.M) {
+      float4 o[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) o[j] = xch[j * 128 + lrow];
+      float M = m;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) M = fmax_nan(M, o[j].x);
+      float S = 0.f;
+      int best = 0x7FFFFFFF;
+      if (M == -INFINITY || M != M) {
+        S = (M != M) ? M : 0.f;
+      } else {
+        S = ssum * ex2((m - M) * kLog2e);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) S += o[j].y * ex2((o[j].x - M) * kLog2e);
+      }
+      if (m == M) best = am;
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (o[j].x == M) best = min(best, __float_as_int(o[j].z));
+      A.gpart[(size_t)p * kMaxRows + row] = make_float4(M, S, __int_as_float(best), 0.f);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // every MMA, commit and remote arrival of the pair is done
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols)
+                 : "memory");
+  }
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+}  // namespace pair
+
 // One warp per row: lane l folds the partials l, l + 32, ... in order, then a fixed butterfly.
 __global__ void __launch_bounds__(256) lopa_lmhead_fold_kernel(const Args A, int G) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -462,6 +753,35 @@ static int grid_for(int device) {
   return n < kMaxGrid ? n : kMaxGrid;
 }
 
+// The CTA-pair kernel serves rows 129..256 unless LOPA_LMH_SINGLE=1 (A/B switch).
+static bool use_pair_kernel() {
+  static const bool on = [] {
+    const char* v = getenv("LOPA_LMH_SINGLE");
+    return !(v && v[0] == '1');
+  }();
+  return on;
+}
+
+// CTA pairs that can be resident at once (one pair per TPC; an SM without a free partner on its
+// TPC stays idle), cached per device.
+static int pair_grid_for(int device) {
+  static std::mutex mu;
+  static int cached[64];
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64) return 0;
+  if (cached[device] == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (num_sms(device) / 2));
+    cfg.blockDim = dim3(pair::kThreads);
+    cfg.dynamicSmemBytes = pair::kSmemBytes;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, pair::lopa_lmhead_pair_kernel, &cfg) != cudaSuccess || n < 1)
+      n = num_sms(device) / 2;
+    cached[device] = n < kMaxGrid ? n : kMaxGrid;
+  }
+  return cached[device];
+}
+
 }  // namespace lmh
 }  // namespace lopa
 
@@ -514,9 +834,12 @@ static int launch_lmhead_chunk(const void* hidden, int64_t ld_hidden, const void
     std::lock_guard<std::mutex> lk(attr_mu);
     if (device < 0 || device >= 64) return LOPA_ERR_UNSUPPORTED;
     if (!attr_done[device]) {
-      const cudaError_t e = cudaFuncSetAttribute(lmh::lopa_lmhead_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)lmh::kSmemBytes);
+      cudaError_t e = cudaFuncSetAttribute(lmh::lopa_lmhead_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)lmh::kSmemBytes);
+      if (e != cudaSuccess) return cuda_status(e);
+      e = cudaFuncSetAttribute(lmh::pair::lopa_lmhead_pair_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lmh::pair::kSmemBytes);
       if (e != cudaSuccess) return cuda_status(e);
       attr_done[device] = true;
     }
@@ -535,10 +858,22 @@ static int launch_lmhead_chunk(const void* hidden, int64_t ld_hidden, const void
   a.n_branches = n_branches;
   a.window = window < 1 ? 1 : window;
   a.row_base = row_base;
-  const int G = lmh::grid_for(device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  lmh::lopa_lmhead_kernel<<<G, lmh::kThreads, lmh::kSmemBytes, s>>>(ma, mb256, mb16, a);
-  cudaError_t e = cudaGetLastError();
+  int G = 0;  // partials per row (CTAs, or CTA pairs)
+  cudaError_t e = cudaSuccess;
+  if (rows > 128 && lmh::use_pair_kernel()) {
+    lmh::pair::BMaps mb;
+    for (int i = 0; i < 4; ++i)
+      if (!lmh::make_map(&mb.b[i], weight, vocab, hidden_dim, ld_weight, 128 >> i)) return LOPA_ERR_CUDA;
+    const int pairs = lmh::pair_grid_for(device);
+    if (pairs < 1) return LOPA_ERR_CUDA;
+    G = pairs;
+    lmh::pair::lopa_lmhead_pair_kernel<<<2 * pairs, lmh::pair::kThreads, lmh::pair::kSmemBytes, s>>>(ma, mb, a);
+  } else {
+    G = lmh::grid_for(device);
+    lmh::lopa_lmhead_kernel<<<G, lmh::kThreads, lmh::kSmemBytes, s>>>(ma, mb256, mb16, a);
+  }
+  e = cudaGetLastError();
   if (e != cudaSuccess) return LOPA_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((rows + 7) / 8);

@@ -178,3 +178,37 @@ def test_lmhead_row_mask(L):
     assert int(st.item()) == 0
     assert torch.equal(c1[sel], c0[sel]) and torch.equal(a1[sel], a0[sel])
     assert torch.isnan(c1[~sel]).all() and (a1[~sel] == -1).all()
+
+
+@pytest.mark.parametrize("N", [16, 48, 112, 144, 240, 256, 272])
+def test_lmhead_pair_tile_widths(L, N):
+    """Rows 129..256 run on CTA pairs (tcgen05 cta_group::2, M = 256).  V = 74·N gives every pair
+    of a B200 tiles of N columns (N = 272: two tiles of 128 + 144), so tile widths of an odd number
+    of 16-column units (computed 16 columns wider, the extra columns ignored) are all exercised."""
+    M, K, V = 256, 64, 74 * N
+    h, W, _ = syngen.lmhead_inputs(N + 3, M, K, V)
+    st = []
+    _check(L, h, W, stats=st)
+    assert np.mean(st) < 1e-4
+
+
+def test_lmhead_pair_planted_columns(L):
+    """Planted logits (row r: 8 at column c_r, 0 elsewhere) through the pair kernel: every argmax is
+    exactly c_r and every conf equals 1 / (1 + (V - 1) e^-8) — a misplaced or duplicated weight
+    row of either CTA's half shows up as a wrong column or a larger sum."""
+    M = K = 256
+    for V in (8200, 18944, 151936 // 4):
+        h = np.zeros((M, K), np.float32)
+        h[np.arange(M), np.arange(M)] = 1.0
+        Wf = np.zeros((V, K), np.float32)
+        c = (np.arange(M) * 7919) % V
+        Wf[c, np.arange(M)] = 8.0
+        hb = (h.view(np.uint32) >> 16).astype(np.uint16)
+        Wb = (Wf.view(np.uint32) >> 16).astype(np.uint16)
+        head = L.LMHead(_dev(Wb), max_rows=256)
+        conf, am, st = head(_dev(hb))
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0
+        assert am.cpu().numpy().tolist() == c.tolist()
+        want = 1.0 / (1.0 + (V - 1) * np.exp(-8.0))
+        assert np.allclose(conf.cpu().numpy(), want, rtol=1e-5)
