@@ -782,6 +782,12 @@ __device__ __forceinline__ unsigned long long k1_gtime() {
 #else
 #define K1TL(idx) ((void)0)
 #endif
+#ifndef LOPA_NO_PREWAIT
+#define LOPA_NO_PREWAIT 0  // A/B: 1 = the first copy waits for the previous kernel (round-1 form)
+#endif
+#ifndef LOPA_PREWAIT_ITEMS
+#define LOPA_PREWAIT_ITEMS 1  // raw items b, G + b, ... copied before the PDL wait (<= kStages)
+#endif
 // A work claim.  LOPA_TMA_ASM_ATOM: one atom instruction whose value is waited for where it is
 // used (atomicAdd is warp-aggregated by the compiler: vote + shuffle of the returned value,
 // which waits for the round trip at the call).
@@ -821,29 +827,12 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     fence_mbar_init();
   }
   for (int q = tid; q < kItemSlots; q += kThreads) icnt[q] = 0;
-  // PDL: wait for the previous kernel's writes (e.g. the previous step's tables) before touching
-  // global inputs, then let the dependent fold/tail kernel launch (it may prefetch the inputs).
-  grid_dep_wait();
-  grid_dep_launch();
-  const Params P = with_device_window(P_arg);  // after the wait: the window was written before
-  const uint32_t stamp = P.ctrs[2] + 1u;          // this launch's partial epoch
-  if (tid == 0) CHMIN(stamp, 6);
-  // ---- work items: (group g, row).  The first item of CTA b, (0, raw row b), is issued before
-  // the row masks arrive (speculatively: a copy of a row that turns out invalid is discarded by
-  // the consumers).  Every other item is numbered over the VALID rows only (masked rows of
-  // present branches, ascending in vlist[0, n_valid)), group-major, without the group-0 items of
-  // rows < G already covered by the speculative copies:
-  //   d < n0:  (0, vlist[lo + d])   (lo = valid rows below G, n0 = n_valid - lo)
-  //   else:    e = d - n0, (1 + e / n_valid, vlist[e % n_valid])
-  // so no claim is ever spent on an unmasked row or an absent branch.  CTA b takes d = b, then
-  // claims d = G + counter, two claims in flight (the first two sent before the masks arrive).
-  const int W = P.window;
-  const int n_seg = P.n_seg, n_grp = P.n_grp;
-  const int G = (int)gridDim.x;
-  const int n_items_cap = P.n_cand * n_grp;
+  const int n_seg = P_arg.n_seg, n_grp = P_arg.n_grp;
   const uint64_t pol = policy_evict_first();
   uint32_t i = 0;  // producer: item (= stage use) sequence number of this CTA
-  // Issue one work item (group g, row): ONE bulk copy of its <= kSegPerItem segments.
+  int n_cand_chk = P_arg.n_cand;
+  // Issue one work item (group g, row): ONE bulk copy of its <= kSegPerItem segments.  Uses only
+  // window-independent fields (logits, ld, segmentation), so it may run before the PDL wait.
   auto issue = [&](int g, int row) {
     const int s0 = g * kSegPerItem, s1 = min(n_seg, s0 + kSegPerItem);
     const int slot = (int)(i % kItemSlots);
@@ -856,16 +845,64 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
 #ifdef LOPA_CHECKED
     stage_seq[s] = i;
 #endif
-    const int e0 = s0 * P.seg_len;
-    const int e1 = min(P.vocab, s1 * P.seg_len);
+    const int e0 = s0 * P_arg.seg_len;
+    const int e1 = min(P_arg.vocab, s1 * P_arg.seg_len);
     const uint32_t bytes = (uint32_t)(((e1 - e0 + 7) >> 3) << 4);
-    LOPA_CHK(row >= 0 && row < P.n_cand && g >= 0 && g < n_grp && (int64_t)e0 + bytes / 2 <= P.ld, 1);
+    LOPA_CHK(row >= 0 && row < n_cand_chk && g >= 0 && g < n_grp && (int64_t)e0 + bytes / 2 <= P_arg.ld, 1);
     mbar_arrive_expect_tx(&full[s], bytes);
-    bulk_g2s(stages + (size_t)s * kStageBytes, P.logits + (size_t)row * P.ld + e0, bytes,
+    bulk_g2s(stages + (size_t)s * kStageBytes, P_arg.logits + (size_t)row * P_arg.ld + e0, bytes,
              &full[s], pol);
     ++i;
   };
   const int b = blockIdx.x;
+  // The first item of CTA b, (0, raw row b), is copied BEFORE the PDL wait when the row count is
+  // a launch argument (no device window): the logits are never written by the kernel this one
+  // waits for (the previous step's K2 writes tables only; a forward that writes them does not
+  // trigger its dependents early), so the copy overlaps the previous kernel's tail — the K2
+  // decisions of the previous step, or the previous launch's last CTAs.
+#ifndef LOPA_NO_SPEC
+  const bool pre_issue = P_arg.window_dev == nullptr && !LOPA_NO_PREWAIT;
+  if (tid == 0 && pre_issue) {
+    if (b < P_arg.n_cand) {
+      issue(0, b);
+    } else if (b < P_arg.n_cand * n_grp) {
+      issue(b / P_arg.n_cand, b % P_arg.n_cand);
+    }
+#pragma unroll 1
+    for (int j = 1; j < LOPA_PREWAIT_ITEMS; ++j) {
+      int r = j * (int)gridDim.x + b, g = 0;
+      if (r >= P_arg.n_cand * n_grp) break;
+      while (r >= P_arg.n_cand) {
+        r -= P_arg.n_cand;
+        ++g;
+      }
+      issue(g, r);
+    }
+  }
+  const int n_spec = pre_issue ? LOPA_PREWAIT_ITEMS : 1;  // raw items [0, n_spec G) are covered
+#else
+  const int n_spec = 0;
+#endif
+  // PDL: wait for the previous kernel's writes (e.g. the previous step's tables) before touching
+  // global inputs, then let the dependent fold/tail kernel launch (it may prefetch the inputs).
+  grid_dep_wait();
+  grid_dep_launch();
+  const Params P = with_device_window(P_arg);  // after the wait: the window was written before
+  n_cand_chk = P.n_cand;
+  const uint32_t stamp = P.ctrs[2] + 1u;          // this launch's partial epoch
+  if (tid == 0) CHMIN(stamp, 6);
+  // ---- work items: (group g, row).  The first item of CTA b, (0, raw row b), is issued before
+  // the row masks arrive (speculatively: a copy of a row that turns out invalid is discarded by
+  // the consumers).  Every other item is numbered over the VALID rows only (masked rows of
+  // present branches, ascending in vlist[0, n_valid)), group-major, without the group-0 items of
+  // rows < G already covered by the speculative copies:
+  //   d < n0:  (0, vlist[lo + d])   (lo = valid rows below G, n0 = n_valid - lo)
+  //   else:    e = d - n0, (1 + e / n_valid, vlist[e % n_valid])
+  // so no claim is ever spent on an unmasked row or an absent branch.  CTA b takes d = b, then
+  // claims d = G + counter, two claims in flight (the first two sent before the masks arrive).
+  const int W = P.window;
+  const int G = (int)gridDim.x;
+  const int n_items_cap = P.n_cand * n_grp;
   uint32_t p1 = 0x7FFFFFFFu, p2 = 0x7FFFFFFFu;
   const bool dyn = G < n_items_cap;  // claims can be needed (the exact test follows the masks)
   if (tid == 0) {
@@ -873,10 +910,12 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
     // raw item b (no division on the common path: the kernel's first instructions are fetched
     // cold at every launch, and an integer-division subroutine there measured +0.35 us)
 #ifndef LOPA_NO_SPEC
-    if (b < P.n_cand) {
-      issue(0, b);
-    } else if (b < n_items_cap) {
-      issue(b / P.n_cand, b % P.n_cand);
+    if (!pre_issue) {
+      if (b < P.n_cand) {
+        issue(0, b);
+      } else if (b < n_items_cap) {
+        issue(b / P.n_cand, b % P.n_cand);
+      }
     }
 #endif
     // the first two claims travel while the masks load
@@ -927,8 +966,8 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
       q = 0;  // experiment: no speculative copy, so no raw item is covered
       const int rq = 0;
 #else
-      q = G / P.n_cand;  // n_cand > 0 here (compact implies 7 n_cand > 8 n_valid >= 0)
-      const int rq = G - q * P.n_cand;
+      q = n_spec * G / P.n_cand;  // n_cand > 0 here (compact implies 7 n_cand > 8 n_valid >= 0)
+      const int rq = n_spec * G - q * P.n_cand;
 #endif
       n_rows = n_valid;
       int base = 0;
@@ -951,7 +990,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
         // raw rows: items b (issued above), G + b, ..., (S - 1) G + b, then S G + counter ...; an
         // invalid row's item is skipped
         const int n_items = P.n_cand * n_grp;
-        const int S = max(2, (int)((int64_t)n_items * kStaticPct / 100) / G);
+        const int S = max(max(2, n_spec), (int)((int64_t)n_items * kStaticPct / 100) / G);
         auto maybe_issue = [&](int cur) {
           const int g = cur / P.n_cand, row = cur - g * P.n_cand;
           if (row_valid(row)) issue(g, row);
@@ -959,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
 #ifdef LOPA_NO_SPEC
         if (b < n_items) maybe_issue(b);  // experiment: item b only after the masks
 #endif
-        for (int jr = 1; jr < S && jr * G + b < n_items; ++jr) maybe_issue(jr * G + b);
+        for (int jr = max(1, n_spec); jr < S && jr * G + b < n_items; ++jr) maybe_issue(jr * G + b);
         if (dyn) {
           while (true) {
             const int c1 = S * G + (int)p1;
