@@ -176,7 +176,13 @@ int lopa_verify_select_ex(const float* conf, const uint8_t* branch_mask, const i
                           float* scores, int32_t* winner, void* stream);
 
 /* One verify step (a1 -> a2 -> a3 -> a4): the streaming reduction kernel and the fold/decision
- * kernel, launched back to back (programmatic dependent launch) on `stream`. */
+ * kernel, launched back to back (programmatic dependent launch) on `stream`.
+ * Stream-order contract for `logits` (all calls that read logits): the reduction kernel starts
+ * copying its first logits rows as soon as the previous kernel on the stream lets dependents
+ * launch (griddepcontrol.launch_dependents; a kernel that never executes it does so at its end),
+ * before waiting for that kernel's memory.  A kernel that writes the logits must therefore not
+ * trigger its dependents before its last logits store (ordinary kernels, copies and liblopa's own
+ * kernels satisfy this). */
 typedef struct {
   /* inputs */
   const void* logits;            /* device bf16 [max_branches][window][ld]: verify logits     */
