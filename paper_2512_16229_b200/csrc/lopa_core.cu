@@ -110,6 +110,16 @@ __device__ __forceinline__ unsigned long long ch_now() {
 #define CHMIN(e, s) atomicMin(&g_chain[(e) & 63][(s)], ch_now())
 #define CHMAX(e, s) atomicMax(&g_chain[(e) & 63][(s)], ch_now())
 #define CHSET(e, s) (g_chain[(e) & 63][(s)] = ch_now())
+#elif defined(LOPA_K2_CYC)
+// experiment: K2's phase boundaries in SM clock cycles (thread 0 only, no K1 marks;
+// scripts/k2_cycles.py)
+__device__ unsigned long long g_chain[64][16];
+#define CHMIN(e, s) ((void)0)
+#define CHMAX(e, s) ((void)0)
+#define CHSET(e, s) (g_chain[(e) & 63][(s)] = (unsigned long long)clock64())
+__device__ uint32_t g_k2cur;  // the step being marked (set by K2 before its decisions)
+#define LOPA_SCORE_MARK(s) \
+  do { if (threadIdx.x == 0) g_chain[g_k2cur & 63][(s)] = (unsigned long long)clock64(); } while (0)
 #else
 #define CHMIN(e, s) ((void)0)
 #define CHMAX(e, s) ((void)0)
@@ -636,6 +646,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
 #else
   cta_scores<NT, S>(T, P, nb, W, warp, lane, P.scores);
 #endif
+  if (tid == 0) CHSET(T.stamp, 0);
   __syncthreads();
   if (tid == 0) TLC(22);
   if (tid == 0) CHSET(T.stamp, 7);
@@ -645,6 +656,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
   if (warp == 0) {
     const float sc = lane < P.cap ? T.scores[lane] : -INFINITY;
     const int w = warp_select(sc, lane, nb);
+    if (lane == 0) CHSET(T.stamp, 1);
     WinRegs<S> r;
 #pragma unroll
     for (int h = 0; h < S; ++h) {
@@ -660,6 +672,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
     for (int h = 0; h < S; ++h) anym |= r.msk[h] != 0;
     const bool any = __any_sync(0xffffffffu, anym);
     if (any) warp_anchor<S>(r, P.tau, P.tau_pos ? T.taus : nullptr, W, lane);
+    if (lane == 0) CHSET(T.stamp, 6);
     int n_mb0 = 0;
 #pragma unroll
     for (int h = 0; h < S; ++h) {
@@ -671,6 +684,7 @@ __device__ void cta_tail_step(const Params& P, TailSmem& T, int tid, int nb) {
                            : 0ull;
       n_mb0 += __popc(__ballot_sync(0xffffffffu, r.msk[h]));
     }
+    if (lane == 0) CHSET(T.stamp, 11);
     if (lane == 0) {
 #ifdef LOPA_K2_DEFER_STORES
       T.best = w;
@@ -830,7 +844,9 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   const int n_seg = P_arg.n_seg, n_grp = P_arg.n_grp;
   const uint64_t pol = policy_evict_first();
   uint32_t i = 0;  // producer: item (= stage use) sequence number of this CTA
-  int n_cand_chk = P_arg.n_cand;
+#ifdef LOPA_CHECKED
+  int n_cand_chk = P_arg.n_cand;  // the row bound LOPA_CHK tests (the device window's, after the wait)
+#endif
   // Issue one work item (group g, row): ONE bulk copy of its <= kSegPerItem segments.  Uses only
   // window-independent fields (logits, ld, segmentation), so it may run before the PDL wait.
   auto issue = [&](int g, int row) {
@@ -888,7 +904,9 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   grid_dep_wait();
   grid_dep_launch();
   const Params P = with_device_window(P_arg);  // after the wait: the window was written before
+#ifdef LOPA_CHECKED
   n_cand_chk = P.n_cand;
+#endif
   const uint32_t stamp = P.ctrs[2] + 1u;          // this launch's partial epoch
   if (tid == 0) CHMIN(stamp, 6);
   // ---- work items: (group g, row).  The first item of CTA b, (0, raw row b), is issued before
@@ -1442,6 +1460,9 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   if (tid == 0) TLC(18);
   __syncthreads();
   if (tid == 0) { TL(7); TLC(19); CHSET(stamp, 3); T.stamp = stamp; }
+#ifdef LOPA_K2_CYC
+  if (tid == 0) g_k2cur = stamp;
+#endif
 #ifdef LOPA_CHAIN_TL
   __syncthreads();
 #endif
@@ -2184,14 +2205,15 @@ extern "C" int lopa_debug_timeline(unsigned long long* out, int n_ctas) {
 
 // Debug (LOPA_CHAIN_TL builds): per-step marks of chained steps ([64][8] ns), then cleared.
 extern "C" int lopa_debug_chain_timeline(unsigned long long* out, int n_words) {
-#ifdef LOPA_CHAIN_TL
-  const int need = 64 * 12;
+#if defined(LOPA_CHAIN_TL) || defined(LOPA_K2_CYC)
+  constexpr int kW = (int)(sizeof(lopa::g_chain[0]) / sizeof(unsigned long long));
+  const int need = 64 * kW;
   if (!out || n_words < need) return -need;
   cudaDeviceSynchronize();
   if (cudaMemcpyFromSymbol(out, lopa::g_chain, sizeof(lopa::g_chain)) != cudaSuccess) return 0;
-  unsigned long long init[64][12];
+  unsigned long long init[64][kW];
   for (int i = 0; i < 64; ++i)
-    for (int j = 0; j < 12; ++j) init[i][j] = (j == 0 || j == 6) ? ~0ull : 0ull;
+    for (int j = 0; j < kW; ++j) init[i][j] = (j == 0 || j == 6) ? ~0ull : 0ull;
   cudaMemcpyToSymbol(lopa::g_chain, init, sizeof(init));
   return need;
 #else

@@ -83,6 +83,9 @@ constexpr int kMetricBottomFraction = 2;  // mean of the ceil(eta * |M_Bj|) lowe
 // with <= W terms the sum stays below 2^ceil(log2 W); the host enforces
 // ceil(log2 W) + 23 + ceil(log2 V) <= 53), so the value equals the oracle's fp64 value whatever
 // the order, rounded once to fp32.  1.0 if M_Bj is empty.
+#ifndef LOPA_SCORE_MARK
+#define LOPA_SCORE_MARK(s) ((void)0)
+#endif
 template <int S>
 __device__ __forceinline__ float warp_metric_score(const float* conf, const uint8_t* mask, int W,
                                                    int metric, float param, double* dscr,
@@ -100,13 +103,17 @@ __device__ __forceinline__ float warp_metric_score(const float* conf, const uint
     n += __popc(b[h]);
   }
   if (n == 0) return 1.0f;
+  LOPA_SCORE_MARK(12);
   if (metric == kMetricMean) {
     double s = 0.0;
 #pragma unroll
     for (int h = 0; h < S; ++h) s += v[h];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    return (float)(s / (double)n);
+    LOPA_SCORE_MARK(13);
+    const float r = (float)(s / (double)n);
+    LOPA_SCORE_MARK(14);
+    return r;
   }
   const uint32_t lt = (1u << lane) - 1u;
   int idx[S];
