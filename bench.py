@@ -132,6 +132,34 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- workload
+def make_branch_parallel(lopa, st, rank, world, dist, dev):
+    """The branch-parallel driver of this rank: the record exchange over peer memory
+    (lopa_bp_step_p2p: K2 stores its record into every peer over NVLink and finishes the step
+    itself) by default at N > 1; LOPA_BP_P2P=0 forces the NCCL all-gather (the default at N = 1,
+    where there is no peer).  If the peer-memory setup fails on any rank, every rank uses NCCL.
+    Returns (driver, note or None)."""
+    want_p2p = os.environ.get("LOPA_BP_P2P", "1" if world > 1 else "0") == "1"
+    bp, note, ok = None, None, False
+    if want_p2p:
+        try:
+            bp = lopa.BranchParallel(st, rank, world, p2p=True)
+            ok = True
+        except Exception as e:  # noqa: BLE001 - reported in the bench line
+            note = f"peer-memory setup failed ({type(e).__name__}: {e}); NCCL all-gather used"
+    if dist is not None and want_p2p:
+        flag = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if ok and int(flag.item()) == 0:
+            bp.close()
+            ok = False
+            note = note or "peer-memory setup failed on another rank; NCCL all-gather used"
+    if not ok:
+        bp = lopa.BranchParallel(st, rank, world, p2p=False)
+    if dist is not None:
+        dist.barrier()  # the first exchange starts together on every rank
+    return bp, note
+
+
 def build_workload(lopa, dev, V, W, k, tau, seed, n_buf, lo=0, hi=None, b_loc=None):
     """Branch states after the initial forward (a0) of a fresh block, and n_buf copies of their
     verify logits (branches [lo, hi) only, padded to b_loc rows when sharded)."""
@@ -413,41 +441,19 @@ def run_lopa(args):
     sptr = ctypes.c_void_p(stream.cuda_stream)
     L = lopa.lib()
 
-    bp = None
-    p2p_note = None
-    if use_bp:
-        # the record exchange over peer memory (lopa_bp_step_p2p: K2 stores its record into every
-        # peer over NVLink and finishes the step itself) by default at N > 1; LOPA_BP_P2P=0 forces
-        # the NCCL all-gather (the default at N = 1, where there is no peer).  If the peer-memory
-        # setup or a first exchange fails, the run falls back to NCCL and says so in the line.
-        want_p2p = os.environ.get("LOPA_BP_P2P", "1" if world > 1 else "0") == "1"
-        ok = False
-        if want_p2p:
-            try:
-                bp = lopa.BranchParallel(st, rank, world, p2p=True)
-                ok = True
-            except Exception as e:  # noqa: BLE001 - reported in the bench line
-                p2p_note = f"peer-memory setup failed ({type(e).__name__}: {e}); NCCL all-gather used"
-        if dist is not None and want_p2p:
-            flag = torch.tensor([1 if ok else 0], device=dev)
-            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-            if ok and int(flag.item()) == 0:
-                bp.close()
-                ok = False
-                p2p_note = p2p_note or "peer-memory setup failed on another rank; NCCL all-gather used"
-        if not ok:
-            bp = lopa.BranchParallel(st, rank, world, p2p=False)
+    bp, p2p_note = (make_branch_parallel(lopa, st, rank, world, dist, dev) if use_bp else (None, None))
 
     # prebuilt argument structs (one per rotating buffer): the timed loop only launches
-    if bp is None:
-        argv = [st.args(b, nb, tok, msk) for b in bufs]
-        refs = [ctypes.byref(a) for a in argv]
+    def make_launch(bp):
+        if bp is None:
+            argv = [st.args(b, nb, tok, msk) for b in bufs]
+            refs = [ctypes.byref(a) for a in argv]
 
-        def launch(i):
-            s = L.lopa_step(refs[i % n_buf], sptr)
-            if s:
-                raise lopa.LopaError(f"lopa_step status {s}")
-    else:
+            def launch(i):
+                s = L.lopa_step(refs[i % n_buf], sptr)
+                if s:
+                    raise lopa.LopaError(f"lopa_step status {s}")
+            return launch, argv
         argv = []
         for b in bufs:
             a = st.args(b, nb, tok, msk)
@@ -465,8 +471,12 @@ def run_lopa(args):
                 s = L.lopa_bp_step(bp.h, refs[i % n_buf], bp.b_loc, rec, sptr)
             if s:
                 raise lopa.LopaError(f"lopa_bp_step status {s}")
+        return launch, argv
 
-    # warm-up
+    launch, argv = make_launch(bp)
+    # warm-up (ranks start it together)
+    if dist:
+        dist.barrier()
     for i in range(args.warmup):
         launch(i)
     torch.cuda.synchronize()
@@ -475,7 +485,18 @@ def run_lopa(args):
         if dist is not None:
             dist.all_reduce(bad, op=dist.ReduceOp.MAX)
         if int(bad.item()):
-            raise RuntimeError("peer-memory exchange timed out during the warm-up; rerun with LOPA_BP_P2P=0")
+            # a peer's record never arrived within the bounded wait: measure the NCCL exchange
+            # instead (and say so in the line) rather than fail the run
+            bp.close()
+            bp = lopa.BranchParallel(st, rank, world, p2p=False)
+            p2p_note = "peer-memory exchange timed out during the warm-up; NCCL all-gather used"
+            st.out.status.zero_()
+            launch, argv = make_launch(bp)
+            if dist:
+                dist.barrier()
+            for i in range(args.warmup):
+                launch(i)
+            torch.cuda.synchronize()
 
     # timed region (headline): K steps back to back, events only at the ends (so the PDL overlap
     # between a step's kernels and the next step's is not broken by interleaved event records)
@@ -870,8 +891,7 @@ def run_loop(args):
     V, W, k, tau, seed, nblk = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["seed"], CFG["loop_blocks"]
     st = lopa.Stepper(V, W, k + 1, k, tau, dev)
     use_bp = world > 1 or os.environ.get("LOPA_BENCH_FORCE_BP") == "1"
-    drv = (lopa.BranchParallel(st, rank, world, p2p=os.environ.get("LOPA_BP_P2P", "1" if world > 1 else "0") == "1")
-           if use_bp else _SingleGPU(st))
+    drv = make_branch_parallel(lopa, st, rank, world, dist, dev)[0] if use_bp else _SingleGPU(st)
     _, lo, hi, _buf = drv.ranks()[0]
     stream = torch.cuda.current_stream(dev)
 

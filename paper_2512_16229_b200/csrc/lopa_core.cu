@@ -1665,8 +1665,9 @@ __device__ bool bp_wait_flags(const Params& P, const uint32_t* flags, int world,
                               int lane) {
   if (lane < world) {
     uint32_t v = 0;
-    // bounded (~0.1-0.2 s): a healthy exchange lands within microseconds
-    for (uint32_t spin = 0; spin < (1u << 21); ++spin) {
+    // bounded (>= 1 s: 2^24 polls 64 ns apart): a healthy exchange lands within microseconds;
+    // the slack absorbs ranks that reach their first step at different times (module loading)
+    for (uint32_t spin = 0; spin < (1u << 24); ++spin) {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + lane) : "memory");
       if (v >= epoch) break;
       __nanosleep(64);
