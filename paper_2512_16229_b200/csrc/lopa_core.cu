@@ -809,10 +809,14 @@ __device__ __forceinline__ unsigned long long k1_gtime() {
 #define LOPA_STATIC_PCT 0
 #endif
 constexpr int kStaticPct = LOPA_STATIC_PCT;  // % of K1's items assigned statically
+#ifndef LOPA_CLAIM_ITEMS
+#define LOPA_CLAIM_ITEMS 1  // items per work claim (one atomic returns this many consecutive items)
+#endif
+constexpr int kClaimItems = LOPA_CLAIM_ITEMS;
 #ifdef LOPA_TMA_ASM_ATOM
-#define K1_CLAIM(p) atom_add_u32((p), 1u)
+#define K1_CLAIM(p) atom_add_u32((p), (uint32_t)kClaimItems)
 #else
-#define K1_CLAIM(p) atomicAdd((p), 1u)
+#define K1_CLAIM(p) atomicAdd((p), (uint32_t)kClaimItems)
 #endif
 __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel(const Params P_arg) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1023,10 +1027,16 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
             if (c1 >= n_items) break;
             p1 = K1_CLAIM(&P.ctrs[0]);
             maybe_issue(c1);
+#pragma unroll
+            for (int u = 1; u < kClaimItems; ++u)
+              if (c1 + u < n_items) maybe_issue(c1 + u);
             const int c2 = S * G + (int)p2;
             if (c2 >= n_items) break;
             p2 = K1_CLAIM(&P.ctrs[0]);
             maybe_issue(c2);
+#pragma unroll
+            for (int u = 1; u < kClaimItems; ++u)
+              if (c2 + u < n_items) maybe_issue(c2 + u);
           }
         }
       } else {
@@ -1052,10 +1062,16 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
             if (c1 >= n_dyn) break;
             p1 = K1_CLAIM(&P.ctrs[0]);
             issue_d(c1);
+#pragma unroll
+            for (int u = 1; u < kClaimItems; ++u)
+              if (c1 + u < n_dyn) issue_d(c1 + u);
             const int c2 = S * G + (int)p2;
             if (c2 >= n_dyn) break;
             p2 = K1_CLAIM(&P.ctrs[0]);
             issue_d(c2);
+#pragma unroll
+            for (int u = 1; u < kClaimItems; ++u)
+              if (c2 + u < n_dyn) issue_d(c2 + u);
           }
         }
       }
