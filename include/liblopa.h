@@ -94,6 +94,11 @@ const char* lopa_status_string(int status);
 /* The CUDA runtime's message for the last call of this thread that returned LOPA_ERR_CUDA
  * ("" if none).  The string is owned by the library and valid until the next such call. */
 const char* lopa_last_cuda_error(void);
+/* Whether the reduction kernel may copy its first logits rows before waiting for the previous
+ * kernel on the stream (see the stream-order contract at lopa_step_args_t): 1 (the default) or
+ * 0, for callers whose logits producer lets its dependents launch before its last logits store.
+ * Process-wide, read at every launch; returns the previous setting. */
+int lopa_set_logits_prefetch(int32_t enabled);
 /* Debug: {registers/thread, max threads/block, static shared bytes, local bytes/thread, block
  * size launched} of the vocabulary-reduction kernel K1 this build uses. */
 int lopa_debug_k1_attrs(int32_t* out5);
@@ -182,7 +187,7 @@ int lopa_verify_select_ex(const float* conf, const uint8_t* branch_mask, const i
  * launch (griddepcontrol.launch_dependents; a kernel that never executes it does so at its end),
  * before waiting for that kernel's memory.  A kernel that writes the logits must therefore not
  * trigger its dependents before its last logits store (ordinary kernels, copies and liblopa's own
- * kernels satisfy this). */
+ * kernels satisfy this), or the caller turns the early copy off: lopa_set_logits_prefetch(0). */
 typedef struct {
   /* inputs */
   const void* logits;            /* device bf16 [max_branches][window][ld]: verify logits     */

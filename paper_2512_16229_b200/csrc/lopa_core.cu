@@ -178,6 +178,7 @@ struct Params {
   int32_t cap;                 // branch capacity of the logits / conf tables
   int32_t table_rows;          // rows of the replicated branch tables (max_branches; n_rows / 1 for a1 alone)
   int32_t k1_alone;            // K1 launched without a consumer (lopa_debug_reduce_only)
+  int32_t prefetch;            // K1 may copy its first item before the PDL wait (lopa_set_logits_prefetch)
   // MODE_BP_FUSED: the peer-memory exchange (lopa_bp_step_p2p)
   uint8_t* const* peer_base;   // device array: every rank's mapped exchange buffer
   int32_t bp_world, bp_rank, bp_b_loc, bp_parity;
@@ -881,7 +882,7 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
   // trigger its dependents early), so the copy overlaps the previous kernel's tail — the K2
   // decisions of the previous step, or the previous launch's last CTAs.
 #ifndef LOPA_NO_SPEC
-  const bool pre_issue = P_arg.window_dev == nullptr && !LOPA_NO_PREWAIT;
+  const bool pre_issue = P_arg.window_dev == nullptr && P_arg.prefetch != 0 && !LOPA_NO_PREWAIT;
   if (tid == 0 && pre_issue) {
     if (b < P_arg.n_cand) {
       issue(0, b);
@@ -1947,10 +1948,14 @@ constexpr size_t kK1Smem = kSmemBytes;
 constexpr int kK1CtasPerSm = LOPA_CTAS_PER_SM;
 #endif
 
+// lopa_set_logits_prefetch: process-wide, read at every launch of K1
+static std::atomic<int> g_logits_prefetch{1};
+
 static int launch_reduce(const Params& P0, int device, cudaStream_t s, bool k1_only = false) {
   int st = ensure_kernel_attrs(device);
   if (st != LOPA_OK) return st;
   Params P = P0;
+  P.prefetch = g_logits_prefetch.load(std::memory_order_relaxed);
   P.k1_alone = k1_only ? 1 : 0;
   if (k1_only) {  // measurement: K1 alone, in the step's launch configuration
     const int g = kK1CtasPerSm * (num_sms(device) - 1);
@@ -2166,6 +2171,10 @@ void lopa::note_cuda_error(cudaError_t e) {
            cudaGetErrorString(e));
 }
 extern "C" const char* lopa_last_cuda_error(void) { return g_last_cuda_error; }
+
+extern "C" int lopa_set_logits_prefetch(int32_t enabled) {
+  return lopa::g_logits_prefetch.exchange(enabled ? 1 : 0);
+}
 
 extern "C" int lopa_profile_enable(int32_t max_records) {
   if (max_records < 1) return LOPA_ERR_INVALID_ARG;

@@ -64,6 +64,7 @@ _SIGS = {
     "lopa_version": (_i32, []),
     "lopa_status_string": (ctypes.c_char_p, [_i32]),
     "lopa_last_cuda_error": (ctypes.c_char_p, []),
+    "lopa_set_logits_prefetch": (_i32, [_i32]),
     "lopa_debug_k1_attrs": (_i32, [ctypes.c_void_p]),
     "lopa_debug_check_read": (_i32, [ctypes.c_void_p]),
     "lopa_d2f_init": (_i32, [_c_void_p, _c_void_p]),
@@ -603,6 +604,13 @@ class DecodeBlockGraphBP:
 
 
 # ----------------------------------------------------------------------------- measurement
+def set_logits_prefetch(enabled: bool) -> bool:
+    """lopa_set_logits_prefetch: allow (default) or forbid K1's first logits copy before the PDL
+    wait (forbid it when the logits producer triggers its dependents early).  Returns the
+    previous setting."""
+    return bool(lib().lopa_set_logits_prefetch(1 if enabled else 0))
+
+
 def profile_enable(max_records: int):
     """Record CUDA events around every K1 (vocabulary reduction) launch of the next calls."""
     _check(lib().lopa_profile_enable(max_records), "lopa_profile_enable")

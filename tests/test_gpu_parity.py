@@ -784,3 +784,33 @@ def test_step_without_branches_passes_through(L):
     torch.cuda.synchronize()
     assert int(o.n_next.item()) == 0 and int(o.winner.item()) == 0 and int(o.status.item()) == 0
     assert torch.equal(o.next_tokens[0], tok[0]) and torch.equal(o.next_mask[0], msk[0])
+
+
+def test_logits_prefetch_switch_bit_identical(L):
+    """lopa_set_logits_prefetch(0) (K1's first copy after the PDL wait) gives the same bits as the
+    default early copy, on the Dream step and through a chained sequence of steps."""
+    import numpy as np
+    V, W, k, tau = 151936, 32, 7, 0.9
+    st = L.Stepper(V, W, k + 1, k, tau, DEV)
+    tok = torch.zeros((k + 1, W), dtype=torch.int32, device=DEV)
+    msk = torch.ones((k + 1, W), dtype=torch.uint8, device=DEV)
+    nb = torch.full((1,), k + 1, dtype=torch.int32, device=DEV)
+    g = torch.Generator(device=DEV).manual_seed(5)
+    logits = [(torch.randn((k + 1, W, st.ld), device=DEV, generator=g) * 2).to(torch.bfloat16)
+              for _ in range(3)]
+    outs = {}
+    for pf in (True, False):
+        prev = L.set_logits_prefetch(pf)
+        try:
+            res = []
+            for x in logits:
+                o = st.step(x, nb, tok, msk)
+                torch.cuda.synchronize()
+                res.append((o.conf.clone(), o.argmax.clone(), o.winner.clone(), o.next_tokens.clone()))
+        finally:
+            L.set_logits_prefetch(prev)
+        outs[pf] = res
+    for a, b in zip(outs[True], outs[False]):
+        for u, v in zip(a, b):
+            assert torch.equal(u.view(torch.int32) if u.dtype == torch.float32 else u,
+                               v.view(torch.int32) if v.dtype == torch.float32 else v)
