@@ -455,7 +455,11 @@ int lopa_bp_commit_winner(lopa_bp_t* bp, const int32_t* winner, int32_t b_loc,
  *            -inf, sets LOPA_DEV_NONFINITE (conf NaN, argmax -1); -inf logits are tokens of
  *            probability 0 (R20)
  *   workspace   lopa_lmhead_workspace_bytes(rows) bytes of device memory (no zeroing needed)
- * Two kernels (tcgen05 GEMM + epilogue, then a fold of the per-SM partials) on `stream`. */
+ * Two kernels (tcgen05 GEMM + epilogue, then a fold of the per-SM partials) on `stream`.
+ * Passes of 129-256 rows run on CTA pairs and are launched programmatically dependent: they
+ * request their first weight rows before the previous kernel on the stream has finished, so
+ * `weight` must not be written by that kernel (it is a model parameter); `hidden` and the
+ * workspace are read / written only after it. */
 size_t lopa_lmhead_workspace_bytes(int32_t rows);
 int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, const void* weight,
                            int64_t ld_weight, int32_t rows, int32_t hidden_dim, int32_t vocab,

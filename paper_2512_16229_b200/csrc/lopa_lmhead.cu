@@ -525,10 +525,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // The weights are constant model parameters: the first stages' weight rows are requested
+  // BEFORE the PDL wait, so they stream while the previous kernel (e.g. the previous step's
+  // decisions) finishes; the hidden states (a previous kernel's output) and the workspace are
+  // touched only after it.
+  const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
+  auto load_b = [&](int s, int kb, int vb, int nh, uint32_t bar) {
+    uint8_t* sb = smem + (size_t)s * kStageBytes + kABytes;
+    int r = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int box = 128 >> i;
+      if (nh & box) {
+        tma_load_2d_pair(sb + r * kBK * 2, &maps_b.b[i], kb * kBK, vb + r, bar, pol_b);
+        r += box;
+      }
+    }
+  };
+#ifndef LOPA_LMH_NO_PREWAIT
+  const int n_pre = n_tiles > 0 ? min(kStages, nk) : 0;  // stages of tile 0 requested early
+#else
+  const int n_pre = 0;  // A/B: every load after the wait
+#endif
+  if (warp == 0 && lane == 0 && n_pre > 0) {
+    int v0, N, Nm;
+    tile_cols_pair(u0, nu, n_tiles, 0, &v0, &N, &Nm);
+    for (int kb = 0; kb < n_pre; ++kb) {
+      if (rank == 0) mbar_arrive_expect_tx(&full[kb], (uint32_t)(2 * kABytes + Nm * kBK * 2));
+      load_b(kb, kb, v0 + (int)rank * (Nm / 2), Nm / 2, map_to_rank(smem_u32(&full[kb]), 0));
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer (both CTAs): this CTA's rows of A and half of the tile's weight rows
-      const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
       uint32_t it = 0;
       for (int t = 0; t < n_tiles; ++t) {
         int v0, N, Nm;
@@ -539,19 +570,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int s = (int)(it % kStages);
           if (it >= (uint32_t)kStages) wait_bounded(&empty[s], ((it / kStages) - 1) & 1);
           uint8_t* sa = smem + (size_t)s * kStageBytes;
-          uint8_t* sb = sa + kABytes;
-          if (rank == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * kABytes + Nm * kBK * 2));
           const uint32_t bar = map_to_rank(smem_u32(&full[s]), 0);
+          const bool pre = it < (uint32_t)n_pre;  // weights already requested before the wait
+          if (rank == 0 && !pre) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * kABytes + Nm * kBK * 2));
           tma_load_2d_pair(sa, &map_a, kb * kBK, (int)rank * 128, bar, pol_a);
-          int r = 0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int box = 128 >> i;
-            if (nh & box) {
-              tma_load_2d_pair(sb + r * kBK * 2, &maps_b.b[i], kb * kBK, vb + r, bar, pol_b);
-              r += box;
-            }
-          }
+          if (!pre) load_b(s, kb, vb, nh, bar);
         }
       }
     }
@@ -868,7 +891,20 @@ static int launch_lmhead_chunk(const void* hidden, int64_t ld_hidden, const void
     const int pairs = lmh::pair_grid_for(device);
     if (pairs < 1) return LOPA_ERR_CUDA;
     G = pairs;
-    lmh::pair::lopa_lmhead_pair_kernel<<<2 * pairs, lmh::pair::kThreads, lmh::pair::kSmemBytes, s>>>(ma, mb, a);
+    // programmatic dependent launch: the CTA pairs become resident and request their first
+    // weight stages while the previous kernel on the stream finishes (see the kernel)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(lmh::pair::kThreads);
+    cfg.dynamicSmemBytes = lmh::pair::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, lmh::pair::lopa_lmhead_pair_kernel, ma, mb, a);
+    if (e != cudaSuccess) return LOPA_ERR_CUDA;
   } else {
     G = lmh::grid_for(device);
     lmh::lopa_lmhead_kernel<<<G, lmh::kThreads, lmh::kSmemBytes, s>>>(ma, mb256, mb16, a);
