@@ -482,14 +482,37 @@ def run_lopa(args):
     torch.cuda.synchronize()
     if bp is not None and bp.p2p:
         bad = torch.tensor([1 if int(st.out.status.item()) & 4 else 0], device=dev)  # PEER_TIMEOUT
+        if not int(bad.item()):
+            # cross-check the peer-memory exchange against the NCCL one on the same step: any
+            # difference on any rank (winner, branch count, next tables, scores) -> NCCL is used
+            o = st.out
+            snap = lambda: [o.winner.clone(), o.n_next.clone(), o.next_tokens.clone(), o.next_mask.clone(),
+                            bp.scores.clone()]
+            r0 = ctypes.byref(argv[0])
+            if L.lopa_bp_step(bp.h, r0, bp.b_loc, ctypes.c_void_p(bp.records.data_ptr()), sptr):
+                raise lopa.LopaError("lopa_bp_step (cross-check) failed")
+            torch.cuda.synchronize()
+            ref = snap()
+            if L.lopa_bp_step_p2p(bp.h, r0, bp.b_loc, sptr):
+                raise lopa.LopaError("lopa_bp_step_p2p (cross-check) failed")
+            torch.cuda.synchronize()
+            got = snap()
+            same = all(torch.equal(x.view(torch.int32) if x.dtype == torch.float32 else x,
+                                   y.view(torch.int32) if y.dtype == torch.float32 else y)
+                       for x, y in zip(ref, got))
+            bad = torch.tensor([0 if same else 2], device=dev)
+            if int(st.out.status.item()) & 4:
+                bad.fill_(1)
         if dist is not None:
             dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if int(bad.item()) == 2:
+            p2p_note = "peer-memory exchange disagreed with the NCCL exchange on the warm-up step; NCCL all-gather used"
         if int(bad.item()):
             # a peer's record never arrived within the bounded wait: measure the NCCL exchange
             # instead (and say so in the line) rather than fail the run
             bp.close()
             bp = lopa.BranchParallel(st, rank, world, p2p=False)
-            p2p_note = "peer-memory exchange timed out during the warm-up; NCCL all-gather used"
+            p2p_note = p2p_note or "peer-memory exchange timed out during the warm-up; NCCL all-gather used"
             st.out.status.zero_()
             launch, argv = make_launch(bp)
             if dist:
