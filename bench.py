@@ -1290,9 +1290,8 @@ def run_lmhead(args):
     import ctypes
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world != 1:
-        print(json.dumps({"error": "lmhead-dream runs on one GPU (no branch-parallel LM head yet)"}))
-        return 0
+    if world > 1 or os.environ.get("LOPA_BENCH_FORCE_BP") == "1":
+        return run_lmhead_bp(args)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     V, W, k, tau, Kd = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["K"]
@@ -1410,6 +1409,156 @@ def run_lmhead(args):
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_lmhead_bp(args):
+    """--config lmhead-* on N GPUs (branch parallelism, lopa_bp_step_lmhead): every rank runs the
+    LM head + Conf on its own branches' hidden-state rows (b_loc * W of them) and the step's
+    exchange and decisions; the same random-init output projection on every rank."""
+    from paper_2512_16229_b200 import lopa
+    import ctypes
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    V, W, k, tau, Kd = CFG["V"], CFG["W"], CFG["k"], CFG["tau"], CFG["K"]
+    st, tok, msk, nb, full, bufs, rows_total, _ = build_workload(lopa, dev, V, W, k, tau, CFG["seed"], 1)
+    del full, bufs
+    bp, p2p_note = make_branch_parallel(lopa, st, rank, world, dist, dev)
+    b_loc, lo, hi = bp.b_loc, bp.lo, bp.hi
+    rows_local = b_loc * W
+    g = torch.Generator(device=dev).manual_seed(CFG["seed"])
+    NW = 2
+    Ws = [(torch.randn(V, Kd, device=dev, generator=g) / Kd ** 0.5).to(torch.bfloat16) for _ in range(NW)]
+    NH = 8
+    rows = (k + 1) * W
+    Hs = []
+    for _ in range(NH):
+        full_h = (torch.randn(rows, Kd, device=dev, generator=g) * 1.5).to(torch.bfloat16)
+        loc = torch.zeros(rows_local, Kd, dtype=torch.bfloat16, device=dev)
+        n_own = max(0, min(hi, k + 1) - lo) * W
+        if n_own:
+            loc[:n_own] = full_h[lo * W: lo * W + n_own]
+        Hs.append(loc)
+    L = lopa.lib()
+    stream = torch.cuda.current_stream(dev)
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    lmh_ws = torch.empty(L.lopa_lmhead_workspace_bytes(rows_local), dtype=torch.uint8, device=dev)
+    P_ = lopa._p
+    argv = []
+    for _ in range(NH):
+        a = st.args(Hs[0], nb, tok, msk)
+        a.conf, a.argmax = bp.conf.data_ptr(), bp.argmax.data_ptr()
+        a.workspace, a.workspace_bytes = bp.ws.data_ptr(), bp.ws.numel()
+        a.scores = bp.scores.data_ptr()
+        argv.append(a)
+    rec = None if bp.p2p else P_(bp.records)
+
+    def launch(i, h=None):
+        s_ = L.lopa_bp_step_lmhead(bp.h, ctypes.byref(argv[i % NH]), b_loc, P_(Hs[i % NH] if h is None else h),
+                                   Kd, P_(Ws[i % NW]), Kd, Kd, rec, P_(lmh_ws), lmh_ws.numel(), sptr)
+        if s_:
+            raise lopa.LopaError(f"lopa_bp_step_lmhead status {s_}")
+
+    if dist:
+        dist.barrier()
+    for i in range(args.warmup):
+        launch(i)
+    torch.cuda.synchronize()
+    if int(st.out.status.item()) != 0:
+        raise lopa.LopaError(f"device status {int(st.out.status.item())} after the warm-up")
+    K = args.steps
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        head_start(stream)
+        t0.record(stream)
+        for i in range(K):
+            launch(i)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    el_ms = t0.elapsed_time(t1)
+    if dist:
+        t = torch.tensor([el_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el_ms = float(t.item())
+    if int(st.out.status.item()) != 0:
+        raise lopa.LopaError(f"device status {int(st.out.status.item())}")
+    # e2e: this rank's hidden-state shard from pinned host memory, results to the host
+    hh = Hs[0].cpu().pin_memory()
+    d_h = torch.empty_like(Hs[0])
+    o = st.out
+    h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory()
+             for t in (o.winner, o.next_tokens, o.next_mask, o.n_next, o.status)]
+    K2 = max(3, min(K, 200))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(K2):
+        d_h.copy_(hh, non_blocking=True)
+        launch(i, d_h)
+        for hbuf, dsrc in zip(h_out, (o.winner, o.next_tokens, o.next_mask, o.n_next, o.status)):
+            hbuf.copy_(dsrc, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    h2d = hh.numel() * 2
+    d2h = sum(t.numel() * t.element_size() for t in h_out)
+    flops = 2.0 * rows_local * Kd * V
+    pk = peaks()
+    peak = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1416.0)))
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        h_full = torch.cat([Hs[0]], 0)
+        cpu = cpu_baseline_lmhead(h_full.view(torch.int16).cpu().numpy().view(np.uint16),
+                                  Ws[0].view(torch.int16).cpu().numpy().view(np.uint16), rows_local)
+    if dist:
+        dist.barrier()
+    line = {
+        "metric": METRIC, "value": K / (el_ms / 1000.0), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": el_ms / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init output projection, Gaussian hidden states; transformer body out of scope)",
+        "config": {"workload": CFG["name"], "rows": rows, "rows_this_rank": rows_local,
+                   "masked_rows": rows_total, "hidden": Kd,
+                   "parallelism": f"bp{world}" + ("-p2p" if bp.p2p else ""),
+                   "bp_exchange": ("peer memory, fused into K2" if bp.p2p else "NCCL all-gather")
+                                  + ("" if p2p_note is None else f" [{p2p_note}]"),
+                   "l2": f"{NW} rotating weight copies ({NW * V * Kd * 2 / 1e9:.2f} GB >= L2)"},
+        "roofline": {"bound": "tensor", "achieved": flops / (el_ms / K / 1000.0) / 1e12, "peak": peak,
+                     "unit": "TFLOP/s", "frac": flops / (el_ms / K / 1000.0) / 1e12 / peak, "traffic": None,
+                     "kernel": "the whole BP step (LM head + Conf on this rank's rows, exchange, decisions)",
+                     "alg_flops_per_launch": flops,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, back to back)"},
+        "clocks": clk.summary(),
+        "gpu_launches": K * (2 * ((rows_local + 255) // 256) + (1 if bp.p2p else 2)),
+        "e2e": {"value": K2 / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": K2, "note": "each rank: its hidden-state shard H2D, results D2H; max over ranks"},
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    bp.close()
+    if dist:
+        dist.destroy_process_group()
     return 0
 
 

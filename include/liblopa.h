@@ -412,6 +412,20 @@ int lopa_bp_p2p_alloc(lopa_bp_t* bp, int32_t window, int32_t b_loc, size_t paylo
 int lopa_bp_p2p_open(lopa_bp_t* bp, const void* all_handles);
 int lopa_bp_step_p2p(lopa_bp_t* bp, const lopa_step_args_t* args, int32_t b_loc, void* stream);
 
+/* The branch-parallel step from hidden states (NEXT-4 with a5; P:293-298 with P:136):
+ * this rank's rows -- branches [rank b_loc, (rank + 1) b_loc), i.e. b_loc * window rows of
+ * `hidden` (device bf16 [b_loc * window][ld_hidden], the rank's slice of the verify forward)
+ * -- through the LM head + Conf (as lopa_lmhead_confidence, into args->conf / args->argmax, the
+ * rank's [b_loc][window] arrays; rows of absent branches are not reduced), then the exchange and
+ * the global a2 -> a4 exactly as lopa_bp_step_p2p (peer memory opened: `records` unused, NULL)
+ * or lopa_bp_step (NCCL: `records` = the [world][lopa_bp_record_bytes] device buffer).
+ * args->logits is not read.  lmh_workspace: lopa_lmhead_workspace_bytes(b_loc * window) bytes.
+ * Same results (bits) as lopa_step_lmhead on one GPU with the same hidden states. */
+int lopa_bp_step_lmhead(lopa_bp_t* bp, const lopa_step_args_t* args, int32_t b_loc,
+                        const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                        int32_t hidden_dim, void* records, void* lmh_workspace,
+                        size_t lmh_workspace_bytes, void* stream);
+
 /* NEXT-3 over peer memory (Commit-Winner-Cache, without a collective): step e's
  * payloads (e.g. each local branch's KV features) are written by their owner into its payload
  * slots of parity e & 1 (lopa_bp_payload_slots: device pointer [b_loc][payload_bytes], NULL if

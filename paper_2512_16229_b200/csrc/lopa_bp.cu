@@ -246,6 +246,48 @@ extern "C" int lopa_bp_step_p2p(lopa_bp_t* bp, const lopa_step_args_t* args, int
 #endif
 }
 
+// The branch-parallel step from hidden states (NEXT-4 x a5): each rank runs the LM head + Conf
+// on its own branches' rows, then the same exchange as lopa_bp_step_p2p (peer memory, when
+// opened) or lopa_bp_step (NCCL all-gather of `records`), the decision kernel reading the
+// LM head's conf / argmax instead of K1's partials.
+extern "C" int lopa_bp_step_lmhead(lopa_bp_t* bp, const lopa_step_args_t* args, int32_t b_loc,
+                                   const void* hidden, int64_t ld_hidden, const void* weight,
+                                   int64_t ld_weight, int32_t hidden_dim, void* records,
+                                   void* lmh_workspace, size_t lmh_workspace_bytes, void* stream) {
+  if (!bp || !args || b_loc < 1 || !hidden || !weight) return LOPA_ERR_INVALID_ARG;
+  if ((int64_t)b_loc * bp->world < args->max_branches) return LOPA_ERR_INVALID_ARG;
+  if (!bp->p2p_open && !records) return LOPA_ERR_INVALID_ARG;
+  if (bp->p2p_open && (b_loc != bp->p2p_b_loc || lopa_bp_record_bytes(args->window, b_loc) != bp->p2p_rb))
+    return LOPA_ERR_INVALID_ARG;
+  if ((int64_t)b_loc * args->window > LOPA_MAX_ROWS) return LOPA_ERR_UNSUPPORTED;
+  if (!args->conf || !args->argmax || !args->dev_status || !args->branch_mask) return LOPA_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int32_t W = args->window;
+  const int32_t base = bp->rank * b_loc;
+  // rows of this rank's branches: branch base + r / W; a row of an absent branch (or one past the
+  // table) is not reduced (conf NaN, argmax -1) and its mask byte is never read
+  int st = lopa::launch_lmhead_rows(hidden, ld_hidden, weight, ld_weight, b_loc * W, hidden_dim,
+                                    args->vocab, args->branch_mask + (size_t)base * W,
+                                    args->n_branches, W, base * W, args->conf, args->argmax,
+                                    args->dev_status, lmh_workspace, lmh_workspace_bytes, stream,
+                                    args->max_branches * W);
+  if (st != LOPA_OK) return st;
+  if (bp->p2p_open) {
+    const uint32_t epoch = ++bp->epoch;
+    const int parity = (int)(epoch & 1u);
+    const size_t rb = bp->p2p_rb;
+    uint8_t* mine = bp->p2p_base + (size_t)parity * bp->world * rb + rb * bp->rank;
+    return lopa::launch_bp_fused(args, b_loc, mine, (uint8_t* const*)bp->d_peer_base, bp->world,
+                                 bp->rank, rb, 2 * (size_t)bp->world * rb, parity, epoch, s, true);
+  }
+  const size_t rb = lopa_bp_record_bytes(W, b_loc);
+  uint8_t* mine = static_cast<uint8_t*>(records) + rb * bp->rank;
+  st = lopa::launch_bp_local(args, base, b_loc, mine, s, true);
+  if (st != LOPA_OK) return st;
+  if (ncclAllGather(mine, records, rb, ncclUint8, bp->comm, s) != ncclSuccess) return LOPA_ERR_NCCL;
+  return lopa::launch_bp_finish(args, b_loc, bp->world, records, s);
+}
+
 // ---- Commit-Winner-Cache over peer memory ---------------------------------------------------------
 namespace {
 // Pull the winner's payload from its owner's mapped payload slots (parity of the last step).

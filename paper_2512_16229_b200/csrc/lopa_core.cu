@@ -179,6 +179,8 @@ struct Params {
   int32_t table_rows;          // rows of the replicated branch tables (max_branches; n_rows / 1 for a1 alone)
   int32_t k1_alone;            // K1 launched without a consumer (lopa_debug_reduce_only)
   int32_t prefetch;            // K1 may copy its first item before the PDL wait (lopa_set_logits_prefetch)
+  int32_t conf_ready;          // K2 without K1: conf / argmax already in P.conf / P.argmax (the
+                               // branch-parallel step from hidden states, lopa_bp_step_lmhead)
   // MODE_BP_FUSED: the peer-memory exchange (lopa_bp_step_p2p)
   uint8_t* const* peer_base;   // device array: every rank's mapped exchange buffer
   int32_t bp_world, bp_rank, bp_b_loc, bp_parity;
@@ -1239,7 +1241,9 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   float4* gst = reinterpret_cast<float4*>(tsm + kTailBytes + LOPA_MAX_ROWS * 2 + 16);
   float4* pscr = gst;  // polling fold's per-thread scratch (the staged copy is unused then)
   const size_t gbytes = (size_t)P.n_grp * P.n_cand * sizeof(float4);
-  const bool staged = MODE != MODE_DECIDE && gbytes <= kGpStageBytes;
+  // conf / argmax come from the previous kernel (the LM head) instead of K1's partials
+  const bool decide_only = MODE == MODE_DECIDE || P.conf_ready != 0;
+  const bool staged = !decide_only && gbytes <= kGpStageBytes;
   if (threadIdx.x == 0 && staged) {
     mbar_init(gbar, 1);
     fence_mbar_init();
@@ -1338,7 +1342,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   const uint32_t stamp = P.ctrs[2] + 1u;  // the epoch K1 stamps (ctrs[2] is constant during K1)
   if (tid == 0) CHSET(stamp, 2);
 #ifndef LOPA_NO_K2_POLL
-  if (MODE != MODE_DECIDE) {
+  if (!decide_only) {
     // Fold every masked row as soon as its n_grp partials of THIS launch have landed (each
     // 64-bit half self-validating, store_partial), while K1 still streams: no grid-wide wait.
     // poll one masked row's n_grp partials and fold them (conf, argmax -> global and T)
@@ -1410,7 +1414,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
     };
     for (int rc = tid; rc < n_masked; rc += kTailThreads) poll_fold_row(rows[rc]);
   } else {
-    grid_dep_wait();  // MODE_DECIDE: conf / argmax written by the previous kernel
+    grid_dep_wait();  // decide only: conf / argmax written by the previous kernel
     for (int rc = tid; rc < n_masked; rc += kTailThreads) {
       const int row = rows[rc];
       T.conf[row] = __ldcg(P.conf + row);
@@ -1421,7 +1425,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
 #else
   grid_dep_wait();  // K1's group partials are visible from here on
   if (tid == 0) { TL(6); TLC(16); }
-  if (MODE == MODE_DECIDE) {
+  if (decide_only) {
     for (int rc = tid; rc < n_masked; rc += kTailThreads) {
       const int row = rows[rc];
       T.conf[row] = __ldcg(P.conf + row);
@@ -1956,6 +1960,10 @@ static int launch_reduce(const Params& P0, int device, cudaStream_t s, bool k1_o
   if (st != LOPA_OK) return st;
   Params P = P0;
   P.prefetch = g_logits_prefetch.load(std::memory_order_relaxed);
+  if (P.conf_ready) {  // no K1: the fold/decision kernel on the previous kernel's conf / argmax
+    auto kern = tail_kernel_for(P.mode, P.window);
+    return cuda_status(launch_pdl(kern, dim3(1), dim3(kTailThreads), kTailSmemBytes, s, P));
+  }
   P.k1_alone = k1_only ? 1 : 0;
   if (k1_only) {  // measurement: K1 alone, in the step's launch configuration
     const int g = kK1CtasPerSm * (num_sms(device) - 1);
@@ -2047,8 +2055,8 @@ static Params base_params(const lopa_step_args_t* a, const Workspace& ws) {
 }
 
 int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_loc, void* record,
-                    cudaStream_t s) {
-  int st = validate_step_args(a, false, true);
+                    cudaStream_t s, bool conf_ready) {
+  int st = validate_step_args(a, false, !conf_ready);
   if (st != LOPA_OK) return st;
   if (!record || b_loc < 1 || branch_base < 0) return LOPA_ERR_INVALID_ARG;
   if (b_loc > LOPA_MAX_BRANCHES || (int64_t)b_loc * a->window > LOPA_MAX_ROWS)
@@ -2057,9 +2065,10 @@ int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_lo
   if (!carve_workspace(a->workspace, a->workspace_bytes, b_loc * a->window, a->vocab, &ws))
     return LOPA_ERR_INVALID_ARG;
   int dev;
-  if (!bind_device(s, a->logits, &dev)) return LOPA_ERR_CUDA;
+  if (!bind_device(s, conf_ready ? static_cast<const void*>(a->conf) : a->logits, &dev)) return LOPA_ERR_CUDA;
   Params P = base_params(a, ws);
   P.mode = MODE_BP_LOCAL;
+  P.conf_ready = conf_ready ? 1 : 0;
   P.branch_base = branch_base;
   P.cap = b_loc;
   P.n_cand = b_loc * a->window;
@@ -2072,8 +2081,8 @@ int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_lo
 // exchange and the global half).  record = this rank's slot of this epoch's parity.
 int launch_bp_fused(const lopa_step_args_t* a, int32_t b_loc, void* record, uint8_t* const* peer_base,
                     int32_t world, int32_t rank, size_t rb, size_t flags_off, int32_t parity,
-                    uint32_t epoch, cudaStream_t s) {
-  int st = validate_step_args(a, true, true);
+                    uint32_t epoch, cudaStream_t s, bool conf_ready) {
+  int st = validate_step_args(a, true, !conf_ready);
   if (st != LOPA_OK) return st;
   if (!record || !peer_base || b_loc < 1 || world < 1 || world > 32 || rank < 0 || rank >= world)
     return LOPA_ERR_INVALID_ARG;
@@ -2083,9 +2092,10 @@ int launch_bp_fused(const lopa_step_args_t* a, int32_t b_loc, void* record, uint
   if (!carve_workspace(a->workspace, a->workspace_bytes, b_loc * a->window, a->vocab, &ws))
     return LOPA_ERR_INVALID_ARG;
   int dev;
-  if (!bind_device(s, a->logits, &dev)) return LOPA_ERR_CUDA;
+  if (!bind_device(s, conf_ready ? static_cast<const void*>(a->conf) : a->logits, &dev)) return LOPA_ERR_CUDA;
   Params P = base_params(a, ws);
   P.mode = MODE_BP_FUSED;
+  P.conf_ready = conf_ready ? 1 : 0;
   P.branch_base = rank * b_loc;
   P.cap = b_loc;
   P.n_cand = b_loc * a->window;

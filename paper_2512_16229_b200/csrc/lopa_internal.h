@@ -54,10 +54,17 @@ inline int cuda_status(cudaError_t e) {
 int launch_bp_finish(const lopa_step_args_t* a, int32_t b_loc, int32_t world, const void* records,
                      cudaStream_t s, const uint32_t* flags = nullptr, uint32_t epoch = 0);
 int launch_bp_local(const lopa_step_args_t* a, int32_t branch_base, int32_t b_loc, void* record,
-                    cudaStream_t s);
+                    cudaStream_t s, bool conf_ready = false);
 int launch_bp_fused(const lopa_step_args_t* a, int32_t b_loc, void* record, uint8_t* const* peer_base,
                     int32_t world, int32_t rank, size_t rb, size_t flags_off, int32_t parity,
-                    uint32_t epoch, cudaStream_t s);
+                    uint32_t epoch, cudaStream_t s, bool conf_ready = false);
+// The LM head + Conf over `rows` rows (chunks of 256); row_base = the global row index of row 0
+// (the n_branches test of the fold), row_mask indexed by the local row.
+int launch_lmhead_rows(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                       int32_t rows, int32_t hidden_dim, int32_t vocab, const uint8_t* row_mask,
+                       const int32_t* n_branches, int32_t window, int32_t row_base, float* conf,
+                       int32_t* argmax, int32_t* dev_status, void* workspace, size_t workspace_bytes,
+                       void* stream, int32_t kernel_rows);
 int validate_step_args(const lopa_step_args_t* a, bool need_next, bool need_logits = true);
 int launch_step_decide(const lopa_step_args_t* a, cudaStream_t s);
 

@@ -704,8 +704,10 @@ __global__ void __launch_bounds__(256) lopa_lmhead_fold_kernel(const Args A, int
   const int row = (int)(blockIdx.x * 8 + (threadIdx.x >> 5));
   const int lane = threadIdx.x & 31;
   if (row >= A.M) return;
-  const bool valid = (!A.row_mask || A.row_mask[row] != 0) &&
-                     (!A.n_branches || (A.row_base + row) / A.window < *A.n_branches);
+  // the branch test first: a row of an absent branch never reads the mask (a shard's rows can
+  // run past the table's last branch)
+  const bool valid = (!A.n_branches || (A.row_base + row) / A.window < *A.n_branches) &&
+                     (!A.row_mask || A.row_mask[row] != 0);
   if (!valid) {  // not a row of the step: untouched semantics of a1 (conf NaN, argmax -1)
     if (lane == 0) {
       A.conf[row] = NAN;
@@ -829,7 +831,7 @@ static int launch_lmhead_chunk(const void* hidden, int64_t ld_hidden, const void
                                int64_t ld_weight, int32_t rows, int32_t hidden_dim, int32_t vocab,
                                const uint8_t* row_mask, const int32_t* n_branches, int32_t window,
                                int32_t row_base, float* conf, int32_t* argmax, int32_t* dev_status,
-                               void* workspace, size_t workspace_bytes, void* stream) {
+                               void* workspace, size_t workspace_bytes, void* stream, bool pair) {
   if (!hidden || !weight || !conf || !argmax || !dev_status || !workspace) return LOPA_ERR_INVALID_ARG;
   if (rows < 1 || rows > lmh::kMaxRows || vocab < 1 || vocab > LOPA_MAX_VOCAB || hidden_dim < lmh::kBK ||
       hidden_dim % lmh::kBK != 0)
@@ -884,7 +886,7 @@ static int launch_lmhead_chunk(const void* hidden, int64_t ld_hidden, const void
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int G = 0;  // partials per row (CTAs, or CTA pairs)
   cudaError_t e = cudaSuccess;
-  if (rows > 128 && lmh::use_pair_kernel()) {
+  if (pair) {
     lmh::pair::BMaps mb;
     for (int i = 0; i < 4; ++i)
       if (!lmh::make_map(&mb.b[i], weight, vocab, hidden_dim, ld_weight, 128 >> i)) return LOPA_ERR_CUDA;
@@ -927,21 +929,38 @@ static int launch_lmhead_chunk(const void* hidden, int64_t ld_hidden, const void
 
 // Rows beyond 256 (e.g. k = 14: 15 branches x 32 positions) run in chunks of 256 rows, each a
 // full pass over the weights (stream-ordered; the workspace is reused).
-static int launch_lmhead(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
-                         int32_t rows, int32_t hidden_dim, int32_t vocab, const uint8_t* row_mask,
-                         const int32_t* n_branches, int32_t window, float* conf, int32_t* argmax,
-                         int32_t* dev_status, void* workspace, size_t workspace_bytes, void* stream) {
-  if (rows < 1 || rows > LOPA_MAX_ROWS || !hidden) return LOPA_ERR_INVALID_ARG;
+namespace lopa {
+int launch_lmhead_rows(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                       int32_t rows, int32_t hidden_dim, int32_t vocab, const uint8_t* row_mask,
+                       const int32_t* n_branches, int32_t window, int32_t row_base, float* conf,
+                       int32_t* argmax, int32_t* dev_status, void* workspace, size_t workspace_bytes,
+                       void* stream, int32_t kernel_rows) {
+  if (rows < 1 || rows > LOPA_MAX_ROWS || !hidden || row_base < 0) return LOPA_ERR_INVALID_ARG;
+  // The kernel form (and so the per-row fold structure, i.e. the conf bits) follows
+  // kernel_rows -- the whole step's rows -- not this call's: a branch-parallel shard reduces its
+  // rows exactly as the one-GPU step does (the CTA pairs serve every pass once the step has more
+  // than 128 rows).
+  const bool pair = (kernel_rows > 128 || rows > 128) && lmh::use_pair_kernel();
   for (int32_t r0 = 0; r0 < rows; r0 += lmh::kMaxRows) {
     const int32_t rc = rows - r0 < lmh::kMaxRows ? rows - r0 : lmh::kMaxRows;
     const int st = launch_lmhead_chunk(
         static_cast<const uint16_t*>(hidden) + (size_t)r0 * ld_hidden, ld_hidden, weight, ld_weight,
-        rc, hidden_dim, vocab, row_mask ? row_mask + r0 : nullptr, n_branches, window, r0,
+        rc, hidden_dim, vocab, row_mask ? row_mask + r0 : nullptr, n_branches, window, row_base + r0,
         conf ? conf + r0 : nullptr, argmax ? argmax + r0 : nullptr, dev_status, workspace,
-        workspace_bytes, stream);
+        workspace_bytes, stream, pair);
     if (st != LOPA_OK) return st;
   }
   return LOPA_OK;
+}
+}  // namespace lopa
+
+static int launch_lmhead(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                         int32_t rows, int32_t hidden_dim, int32_t vocab, const uint8_t* row_mask,
+                         const int32_t* n_branches, int32_t window, float* conf, int32_t* argmax,
+                         int32_t* dev_status, void* workspace, size_t workspace_bytes, void* stream) {
+  return lopa::launch_lmhead_rows(hidden, ld_hidden, weight, ld_weight, rows, hidden_dim, vocab,
+                                  row_mask, n_branches, window, 0, conf, argmax, dev_status,
+                                  workspace, workspace_bytes, stream, rows);
 }
 
 extern "C" int lopa_lmhead_confidence(const void* hidden, int64_t ld_hidden, const void* weight,

@@ -106,6 +106,8 @@ _SIGS = {
     "lopa_bp_commit_winner_p2p": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "lopa_bp_p2p_open": (_i32, [_c_void_p, _c_void_p]),
     "lopa_bp_step_p2p": (_i32, [_c_void_p, ctypes.POINTER(StepArgs), _i32, _c_void_p]),
+    "lopa_bp_step_lmhead": (_i32, [_c_void_p, ctypes.POINTER(StepArgs), _i32, _c_void_p, _i64,
+                                   _c_void_p, _i64, _i32, _c_void_p, _c_void_p, _size, _c_void_p]),
     "lopa_bp_commit_winner": (_i32, [_c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p, _c_void_p]),
     "lopa_bp_destroy": (None, [_c_void_p]),
     "lopa_debug_timeline": (_i32, [_c_void_p, _i32]),
@@ -735,6 +737,31 @@ class BranchParallel:
         else:
             _check(lib().lopa_bp_step(self.h, ctypes.byref(a), self.b_loc, _p(self.records),
                                       _stream(s.device)), "lopa_bp_step")
+        return s.out
+
+    def step_lmhead(self, hidden_local: torch.Tensor, weight: torch.Tensor, n_branches,
+                    branch_tokens, branch_mask) -> StepOutputs:
+        """The step from hidden states (lopa_bp_step_lmhead): this rank's [b_loc * W][K] bf16 hidden
+        rows through the LM head + Conf, then the exchange and the global decisions; weight is the
+        bf16 [V][K] output projection.  Same results as LMHead.step on one GPU."""
+        _need_cuda(hidden_local, weight, n_branches, branch_tokens, branch_mask)
+        s = self.s
+        h = hidden_local.reshape(-1, hidden_local.shape[-1])
+        if h.dtype != torch.bfloat16 or h.stride(1) != 1 or h.shape[0] != self.b_loc * s.window:
+            raise LopaError("hidden_local must be bf16 [b_loc * window][K] with unit inner stride")
+        if weight.dtype != torch.bfloat16 or weight.stride(1) != 1 or tuple(weight.shape) != (s.vocab, h.shape[1]):
+            raise LopaError("weight must be bf16 [V][K] with unit inner stride")
+        if getattr(self, "_lmh_ws", None) is None:
+            self._lmh_ws = torch.empty(lib().lopa_lmhead_workspace_bytes(self.b_loc * s.window),
+                                       dtype=torch.uint8, device=s.device)
+        a = s.args(h, n_branches, branch_tokens, branch_mask)
+        a.conf, a.argmax = self.conf.data_ptr(), self.argmax.data_ptr()
+        a.workspace, a.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
+        a.scores = self.scores.data_ptr()
+        _check(lib().lopa_bp_step_lmhead(self.h, ctypes.byref(a), self.b_loc, _p(h), h.stride(0),
+                                         _p(weight), weight.stride(0), h.shape[1],
+                                         None if self.p2p else _p(self.records), _p(self._lmh_ws),
+                                         self._lmh_ws.numel(), _stream(s.device)), "lopa_bp_step_lmhead")
         return s.out
 
     def commit_winner(self, local_payloads: torch.Tensor, out: torch.Tensor | None = None,

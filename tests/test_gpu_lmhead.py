@@ -212,3 +212,46 @@ def test_lmhead_pair_planted_columns(L):
         assert am.cpu().numpy().tolist() == c.tolist()
         want = 1.0 / (1.0 + (V - 1) * np.exp(-8.0))
         assert np.allclose(conf.cpu().numpy(), want, rtol=1e-5)
+
+
+@pytest.mark.parametrize("p2p", [False, True])
+@pytest.mark.parametrize("seed,V,K,W,k", [(0, 5000, 128, 32, 7), (1, 20000, 256, 16, 3),
+                                          (5, 8000, 128, 32, 14)])
+def test_bp_step_lmhead_matches_one_gpu(L, p2p, seed, V, K, W, k):
+    """lopa_bp_step_lmhead (one rank: the LM head on the shard's rows, then the NCCL or the
+    fused peer-memory exchange with the decisions reading the LM head's conf) gives the same bits
+    as lopa_step_lmhead (oracle-checked in test_step_lmhead): winner, scores, spawned tables,
+    the rows' conf / argmax — including an absent last branch."""
+    rng = np.random.default_rng(seed)
+    nbr = k + 1
+    h, Wt, _ = syngen.lmhead_inputs(seed, nbr * W, K, V)
+    tok = torch.from_numpy(rng.integers(0, V, size=(nbr, W)).astype(np.int32)).to(DEV)
+    m_np = (rng.random((nbr, W)) < 0.7).astype(np.uint8)
+    m_np[:, 0] = 1
+    msk = torch.from_numpy(m_np).to(DEV)
+    n = nbr - 1 if seed % 2 else nbr
+    nb = torch.tensor([n], dtype=torch.int32, device=DEV)
+    hd, wd = _dev(h), _dev(Wt)
+    st1 = L.Stepper(V, W, nbr, k, 0.9, DEV)
+    o1 = L.LMHead(wd).step(st1, hd, nb, tok, msk)
+    torch.cuda.synchronize()
+    ref = {key: getattr(o1, key).clone() for key in ("winner", "n_next", "next_tokens", "next_mask", "scores", "status")}
+    ref_conf, ref_amax = o1.conf.clone(), o1.argmax.clone()
+    st2 = L.Stepper(V, W, nbr, k, 0.9, DEV)
+    bp = L.BranchParallel(st2, 0, 1, p2p=p2p)
+    try:
+        o2 = bp.step_lmhead(hd, wd, nb, tok, msk)
+        torch.cuda.synchronize()
+        assert int(o2.status.item()) == int(ref["status"].item()) == 0
+        assert int(o2.winner.item()) == int(ref["winner"].item())
+        nn = int(o2.n_next.item())
+        assert nn == int(ref["n_next"].item())
+        assert torch.equal(o2.next_tokens[:nn], ref["next_tokens"][:nn])
+        assert torch.equal(o2.next_mask[:nn], ref["next_mask"][:nn])
+        assert torch.equal(bp.scores[:nbr].view(torch.int32), ref["scores"][:nbr].view(torch.int32))
+        sel = torch.from_numpy(m_np.astype(bool)).to(DEV)
+        sel[n:] = False
+        assert torch.equal(bp.conf[sel].view(torch.int32), ref_conf[sel].view(torch.int32))
+        assert torch.equal(bp.argmax[sel], ref_amax[sel])
+    finally:
+        bp.close()
