@@ -1187,6 +1187,9 @@ __global__ void __launch_bounds__(kThreads, LOPA_CTAS_PER_SM) lopa_reduce_kernel
 #endif
 #endif
 constexpr int kTailThreads = LOPA_TAIL_THREADS;
+#ifndef LOPA_POLL_MAX_ROWS
+#define LOPA_POLL_MAX_ROWS (1 << 30)  // masked rows up to which K2 folds by polling (A/B knob)
+#endif
 // K1's group partials are pulled into K2's shared memory with ONE bulk copy when they fit
 // (the Dream step: 10 groups x 256 rows x 16 B = 41 KB): a single L2 round trip instead of
 // ten loads per thread.
@@ -1342,7 +1345,12 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
   const uint32_t stamp = P.ctrs[2] + 1u;  // the epoch K1 stamps (ctrs[2] is constant during K1)
   if (tid == 0) CHSET(stamp, 2);
 #ifndef LOPA_NO_K2_POLL
-  if (!decide_only) {
+  // Polling fold while K1 streams (every step size by default).  The wait-then-fold path below
+  // (K1's grid first, then two rows per thread with every load in flight) is the A/B
+  // alternative for wide steps (LOPA_POLL_MAX_ROWS=256): measured slower at 481-1945 rows
+  // (profiles/r02_k2_phases.md).
+  const bool poll = n_masked <= LOPA_POLL_MAX_ROWS;
+  if (!decide_only && poll) {
     // Fold every masked row as soon as its n_grp partials of THIS launch have landed (each
     // 64-bit half self-validating, store_partial), while K1 still streams: no grid-wide wait.
     // poll one masked row's n_grp partials and fold them (conf, argmax -> global and T)
@@ -1413,12 +1421,62 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
         T.amax[row] = (int32_t)f.a;
     };
     for (int rc = tid; rc < n_masked; rc += kTailThreads) poll_fold_row(rows[rc]);
-  } else {
+  } else if (decide_only) {
     grid_dep_wait();  // decide only: conf / argmax written by the previous kernel
     for (int rc = tid; rc < n_masked; rc += kTailThreads) {
       const int row = rows[rc];
       T.conf[row] = __ldcg(P.conf + row);
       T.amax[row] = __ldcg(P.argmax + row);
+    }
+  } else {
+    grid_dep_wait();  // K1's group partials are final and visible from here on
+    // two rows per thread per round, all of their partials' loads in flight together (a wide
+    // window has several rows per thread: their L2 round trips overlap instead of adding up)
+    auto finish_row = [&](int row, const FoldAcc& f) {
+      LOPA_CHK(row < P.n_cand, 7);
+      const float c = __fdiv_rn(1.0f, f.S);
+      P.conf[row] = c;
+      P.argmax[row] = (int32_t)f.a;
+      if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
+      T.conf[row] = c;
+      T.amax[row] = (int32_t)f.a;
+    };
+    for (int rc = tid; rc < n_masked; rc += 2 * kTailThreads) {
+      const int rc2 = rc + kTailThreads;
+      const int row0 = rows[rc], row1 = rc2 < n_masked ? rows[rc2] : -1;
+      if (n_grp <= 16) {
+        float4 q0[16], q1[16];
+        uint32_t st_bad = 0;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          q0[p] = q1[p] = make_float4(-INFINITY, 0.f, __uint_as_float(0xFFFFFFFFu), 0.f);
+          if (p < n_grp) {
+            uint64_t A, B, A1, B1;
+            load_partial_raw(P.gpart + row0 + (size_t)p * P.n_cand, &A, &B);
+            if (row1 >= 0) load_partial_raw(P.gpart + row1 + (size_t)p * P.n_cand, &A1, &B1);
+            st_bad |= stamped(A, B, stamp) ? 0u : 1u;
+            q0[p] = decode_partial(A, B);
+            if (row1 >= 0) {
+              st_bad |= stamped(A1, B1, stamp) ? 0u : 1u;
+              q1[p] = decode_partial(A1, B1);
+            }
+          }
+        }
+        LOPA_CHK(!st_bad, 6);
+        if (st_bad) atomicOr(P.dev_status, kDevInternal);
+        finish_row(row0, fold_tree16(n_grp, q0));
+        if (row1 >= 0) finish_row(row1, fold_tree16(n_grp, q1));
+      } else {
+        for (int rr = 0; rr < 2; ++rr) {
+          const int row = rr ? row1 : row0;
+          if (row < 0) continue;
+          finish_row(row, fold_seq(n_grp, [&](int p) {
+            uint64_t A, B;
+            load_partial_raw(P.gpart + row + (size_t)p * P.n_cand, &A, &B);
+            return decode_partial(A, B);
+          }));
+        }
+      }
     }
   }
   if (tid == 0) { TL(6); TLC(16); }
