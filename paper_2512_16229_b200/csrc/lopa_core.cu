@@ -1420,6 +1420,72 @@ __global__ void __launch_bounds__(kTailThreads, 1) lopa_tail_kernel(const Params
         T.conf[row] = c;
         T.amax[row] = (int32_t)f.a;
     };
+#ifndef LOPA_NO_PAIR_POLL
+    // Wide steps (more masked rows than threads) with <= 10 groups per row: each thread polls TWO
+    // rows at once (rows rc and rc + threads), their decoded partials kept in three planes
+    // (m, s, argmax) of the scratch, [20][threads] each -- so a thread's second row no longer
+    // waits behind its first.  Same fold (the 16-slot tree), same bits.
+    constexpr int kPS = 10;
+    if (n_masked > kTailThreads && n_grp <= kPS) {
+      float* px = reinterpret_cast<float*>(pscr);
+      float* py = px + 2 * kPS * kTailThreads;
+      uint32_t* pz = reinterpret_cast<uint32_t*>(py + 2 * kPS * kTailThreads);
+      const uint32_t full = (1u << n_grp) - 1u;
+      for (int rc = tid; rc < n_masked; rc += 2 * kTailThreads) {
+        const int rr[2] = {rows[rc], rc + kTailThreads < n_masked ? rows[rc + kTailThreads] : -1};
+        uint32_t pend = full | (rr[1] >= 0 ? full << 16 : 0u);
+        for (uint32_t spin = 0;; ++spin) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            if (!((pend >> (16 * r)) & full)) continue;
+            const float4* q = P.gpart + rr[r];
+            uint64_t A[kPS], B[kPS];
+#pragma unroll
+            for (int p = 0; p < kPS; ++p)
+              if ((pend >> (16 * r + p)) & 1u) load_partial_raw(q + (size_t)p * P.n_cand, &A[p], &B[p]);
+#pragma unroll
+            for (int p = 0; p < kPS; ++p)
+              if (((pend >> (16 * r + p)) & 1u) && stamped(A[p], B[p], stamp)) {
+                const float4 d = decode_partial(A[p], B[p]);
+                const int sl = (r * kPS + p) * kTailThreads + tid;
+                px[sl] = d.x;
+                py[sl] = d.y;
+                pz[sl] = __float_as_uint(d.z);
+                pend &= ~(1u << (16 * r + p));
+              }
+          }
+          if (!pend) break;
+          if (spin >= kPollSpins) {
+            atomicOr(P.dev_status, kDevInternal);
+            LOPA_CHK(false, 6);
+            break;
+          }
+          __nanosleep(64);
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          if (rr[r] < 0) continue;
+          float4 qr[16];
+#pragma unroll
+          for (int p = 0; p < 16; ++p) {
+            const int sl = (r * kPS + p) * kTailThreads + tid;
+            qr[p] = (p < n_grp && !((pend >> (16 * r + p)) & 1u))
+                        ? make_float4(px[sl], py[sl], __uint_as_float(pz[sl]), 0.f)
+                        : make_float4(-INFINITY, 0.f, __uint_as_float(0xFFFFFFFFu), 0.f);
+          }
+          const FoldAcc f = fold_tree16(n_grp, qr);
+          const int row = rr[r];
+          LOPA_CHK(row < P.n_cand, 7);
+          const float cf = __fdiv_rn(1.0f, f.S);
+          P.conf[row] = cf;
+          P.argmax[row] = (int32_t)f.a;
+          if (!(f.S >= 1.0f)) atomicOr(P.dev_status, kDevNonfinite);
+          T.conf[row] = cf;
+          T.amax[row] = (int32_t)f.a;
+        }
+      }
+    } else
+#endif
     for (int rc = tid; rc < n_masked; rc += kTailThreads) poll_fold_row(rows[rc]);
   } else if (decide_only) {
     grid_dep_wait();  // decide only: conf / argmax written by the previous kernel
