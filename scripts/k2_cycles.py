@@ -11,7 +11,8 @@ import bench  # noqa: E402
 from paper_2512_16229_b200 import lopa  # noqa: E402
 
 dev = torch.device("cuda:0")
-st, tok, msk, nb, full, bufs, rows, _ = bench.build_workload(lopa, dev, 151936, 32, 7, 0.9, 1, 8)
+W_, K_ = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (32, 7)
+st, tok, msk, nb, full, bufs, rows, _ = bench.build_workload(lopa, dev, 151936, W_, K_, 0.9, 1, 8)
 L = lopa.lib()
 buf = np.zeros(2048, dtype=np.uint64)
 nw = L.lopa_debug_chain_timeline(buf.ctypes.data, 2048)
